@@ -1,0 +1,201 @@
+/*
+ * tn.h -- C ABI of the B200-native tensor-network contraction engine
+ * (arxiv 2208.01498, Wahl & Strelchuk: separator-based contraction orders for
+ * quantum-circuit amplitudes <x|C|0>).
+ *
+ * Four calls form the boundary named in BASELINE.json's north_star:
+ *   tn_build_network  circuit -> closed tensor network
+ *   tn_find_order     separator hierarchy -> pairwise order  (PAPER.md l.79-96,
+ *                     SM Algorithm 1 l.195-209, SM l.217) + index slicing (l.178)
+ *   tn_contract       order + bitstring -> scalar amplitude  (Eq. (3), l.82-86)
+ *   tn_amplitudes     batch of bitstrings -> amplitudes
+ * plus the hot operation itself, exported for step-level parity tests:
+ *   tn_contract_pair  one pairwise contraction (Fig. 1b, l.54) on device buffers.
+ *
+ * Conventions
+ *   - Every function returns TN_OK (0) or a positive error code; tn_last_error()
+ *     gives a thread-local message.  Nothing aborts the process; on error no output
+ *     is written and no handle is created.
+ *   - Complex numbers are interleaved (re, im) pairs: complex128 = 2 doubles,
+ *     complex64 = 2 floats.  Tensors are dense, row-major over their index list
+ *     (last index fastest).  Index dimensions are powers of two.
+ *   - Handles (tn_network, tn_order, tn_plan) are owned by the caller and released
+ *     with the matching *_free; a network must outlive orders and plans made from it.
+ *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA global
+ *     memory on the plan's device.  Streams are cudaStream_t passed as void*
+ *     (NULL = legacy default stream).
+ *   - There is no CPU fallback: without a usable sm_100 device every device call
+ *     returns TN_ECUDA.
+ */
+#ifndef TN_H_
+#define TN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TN_OK = 0,
+  TN_EINVAL = 1,        /* bad argument (null pointer, out-of-range id, bad layout) */
+  TN_ECUDA = 2,         /* CUDA runtime / driver error or no sm_100 device */
+  TN_ENOMEM = 3,        /* device arena does not fit the plan's budget */
+  TN_EUNSUPPORTED = 4,  /* valid request outside what the engine implements */
+  TN_EINTERNAL = 5
+};
+
+enum { TN_C64 = 0, TN_C128 = 1 };               /* arithmetic type of a plan */
+enum { TN_PATH_AUTO = 0, TN_PATH_SMALL = 1, TN_PATH_TC = 2 };
+
+typedef struct tn_network_s* tn_network;
+typedef struct tn_order_s* tn_order;
+typedef struct tn_plan_s* tn_plan;
+
+const char* tn_last_error(void);
+const char* tn_version(void);
+
+/* ------------------------------------------------------------------ network --
+ * tn_build_network: the closed tensor network of <x|C|0> for a circuit of single-
+ * and two-qubit gates (PAPER.md "Classical Simulation of Quantum Circuits",
+ * l.115-125).  Single-qubit gates and the |0> inputs are absorbed into the two-
+ * qubit gate tensors (l.116); each two-qubit gate is split into two rank-3 tensors
+ * joined by a bond of dimension <= 4 (Theorem 2 proof, l.122) placed at
+ * x_i + (x_j - x_i)/4 and x_j + (x_i - x_j)/4 with radius l/4 + eps.  The output
+ * projections <x_q| stay open legs (one per qubit) until a bitstring is bound.
+ *   n_qubits     N >= 1
+ *   qubit_xy     host, N x 2 doubles: qubit positions in R^2
+ *   n_gates      G >= 0, applied in order
+ *   gate_qubits  host, G x 2 int32: (a, -1) for a one-qubit gate, (a, b) a != b
+ *   gate_mats    host, concatenated row-major complex128 matrices: 2x2 (8 doubles)
+ *                for one-qubit gates, 4x4 (32 doubles) in basis |x_a x_b> (x_a the
+ *                high bit) for two-qubit gates
+ *   diag_hyper   0: paper's construction; 1: diagonal gates keep their wire index
+ *                (hyperedge reading R3 of DESIGN.md, used for IQP circuits)
+ *   out          receives the new handle
+ */
+int tn_build_network(int32_t n_qubits, const double* qubit_xy, int32_t n_gates,
+                     const int32_t* gate_qubits, const double* gate_mats, int32_t diag_hyper,
+                     tn_network* out);
+void tn_network_free(tn_network net);
+
+typedef struct {
+  int32_t n_tensors, n_indices, n_qubits, max_rank;
+  double radius, k_bound;
+} tn_network_info;
+int tn_network_get_info(tn_network net, tn_network_info* info);
+/* dims: host int32[n_indices]; out_legs: host int32[n_qubits] (index id of qubit q's
+ * open output leg) */
+int tn_network_dims(tn_network net, int32_t* dims, int32_t* out_legs);
+/* tensor t: rank, its index ids (host int32[max_rank]), position (2 doubles) and,
+ * if data != NULL, its complex128 entries (data_cap doubles available). */
+int tn_network_tensor(tn_network net, int32_t t, int32_t* rank, int32_t* inds, double* pos,
+                      double* data, int64_t data_cap);
+
+/* ------------------------------------------------------------------- order ---
+ * tn_find_order: recursive sphere-separator bisection of the tensors' embedding
+ * (SM Algorithm 1 steps 1-7; Theorem 1 proof boundary assignment), greedy order
+ * inside leaf clusters of <= leaf_size tensors (SM l.217), the randomized hierarchy
+ * built n_seeds times keeping the smallest Eq. (3) total; then, if
+ * max_log2_size > 0, greedy index slicing until no tensor of the contraction has
+ * more than max_log2_size index bits.  Deterministic in (network, params, seed) and
+ * bit-identical to oracle/ssa.py.
+ */
+typedef struct {
+  int32_t leaf_size;      /* default 8 */
+  int32_t a_max;          /* centerpoint sample size, default 32 */
+  int32_t n_valid;        /* valid circles compared per separator, default 64 */
+  int32_t max_tries;      /* circles per centerpoint, default 256 */
+  int32_t n_seeds;        /* hierarchies built, default 4 */
+  int32_t max_log2_size;  /* slicing target in index bits, <= 0: no slicing */
+} tn_order_params;
+void tn_order_params_default(tn_order_params* p);
+int tn_find_order(tn_network net, const tn_order_params* params, uint64_t seed, tn_order* out);
+void tn_order_free(tn_order ord);
+
+typedef struct {
+  int32_t n_steps, n_slices;           /* n_slices = number of sliced indices */
+  int32_t max_step_log2, max_size_log2; /* unsliced: max log2 M, max log2 result size */
+  int32_t median_fallbacks;
+  double log2_total_2M;                 /* log2 sum_k 2 M_k, unsliced (Eq. (3)) */
+  double log2_slice_2M;                 /* log2 sum_k 2 M_k of one slice */
+  int64_t n_slice_assignments;          /* prod of sliced dimensions */
+} tn_order_info;
+int tn_order_get_info(tn_order ord, tn_order_info* info);
+/* steps: host int32[2 * n_steps] (a, b) pairs; leaves are tensor ids 0..n-1 and
+ * step k creates node n + k.  slices: host int32[n_slices]. */
+int tn_order_steps(tn_order ord, int32_t* steps);
+int tn_order_slices(tn_order ord, int32_t* slices);
+
+/* -------------------------------------------------------------------- plan ---
+ * tn_plan_create: device execution plan for (network, order) in complex64 or
+ * complex128 on CUDA device `device`: uploads the leaf tensors, assigns every
+ * intermediate an offset in one device arena (reused across the tree, slices and
+ * bitstrings), chooses the kernel path of every step (warp-level batched small
+ * kernel vs tensor-core GEMM) and captures the launch sequence of one slice.
+ */
+int tn_plan_create(tn_network net, tn_order ord, int32_t dtype, int32_t device, tn_plan* out);
+void tn_plan_free(tn_plan plan);
+
+typedef struct {
+  double flops_per_slice;        /* 8 * sum_k M_k (real flops of complex MACs) */
+  int64_t n_slices;              /* slice assignments */
+  int64_t arena_bytes;           /* device arena size */
+  int32_t n_steps_small, n_steps_tc, n_launches_per_slice;
+  double tc_flops_per_slice;     /* part of flops_per_slice on the tensor-core path */
+} tn_plan_info;
+int tn_plan_get_info(tn_plan plan, tn_plan_info* info);
+
+/* tn_plan_steps: per step k (order of tn_order_steps), 6 int32 in out[6k..6k+5]:
+ * path (TN_PATH_SMALL / TN_PATH_TC), log2 batch, log2 M, log2 N, log2 K (the GEMM
+ * shape C[b][m][n] = sum_k A[b][m][k] B[b][k][n] as executed), launch position. */
+int tn_plan_steps(tn_plan plan, int32_t* out);
+
+/* tn_contract: amplitude contribution of slices [slice_begin, slice_end) for one
+ * bitstring (bits: host uint8[n_qubits], 0/1).  amp: host double[2] receives the
+ * sum (complex128 regardless of the plan's dtype).  Synchronizes `stream`. */
+int tn_contract(tn_plan plan, const uint8_t* bits, int64_t slice_begin, int64_t slice_end,
+                double* amp, void* stream);
+/* tn_contract_device: same, asynchronous; bits_dev: device uint8[n_qubits];
+ * amp_dev: device complex (plan dtype) accumulator, the sum is ADDED to it. */
+int tn_contract_device(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin,
+                       int64_t slice_end, void* amp_dev, void* stream);
+/* tn_contract_profiled: as tn_contract_device, but launches eagerly (no graph) with
+ * CUDA events around every launch on `stream`; prof (host) receives the summed
+ * device time per kernel class and the algorithmic flops of the GEMM launches. */
+typedef struct {
+  double ms_small, ms_pack, ms_gemm, ms_other;
+  double flops_gemm, flops_small;          /* 8 * M (real flops of the complex MACs) */
+  double bytes_small, bytes_pack;          /* algorithmic bytes read + written */
+  int64_t n_gemm, n_pack, n_small, n_other;
+} tn_profile;
+int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end,
+                         void* amp_dev, void* stream, tn_profile* prof);
+/* tn_amplitudes: full amplitudes (all slices) of n_bits bitstrings
+ * (host uint8[n_bits * n_qubits]) into host double[2 * n_bits]; host<->device
+ * copies included.  Synchronizes `stream`. */
+int tn_amplitudes(tn_plan plan, const uint8_t* bits, int32_t n_bits, double* amps, void* stream);
+
+/* ---------------------------------------------------------------- hot op ----
+ * tn_contract_pair: C = sum over shared non-output indices of A * B (PAPER.md
+ * Fig. 1b, l.54; cost M of Eq. (3)).  An index present in A, B and C is a batch
+ * (hyperedge) index; every index of A and of B must appear in the other operand or
+ * in C, and every index of C in A or B.  A, B, C: device buffers of `dtype`,
+ * row-major over their index lists; dims[i] is the dimension of index id i
+ * (0 <= i < n_dims, powers of two).  path: TN_PATH_AUTO picks the kernel like a
+ * plan does; TN_PATH_SMALL / TN_PATH_TC force one (TN_PATH_TC requires complex64).
+ * Asynchronous on `stream`; scratch memory is taken from an internal pool.
+ */
+int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t* inds_a,
+                     const void* B, int32_t rank_b, const int32_t* inds_b, void* C,
+                     int32_t rank_c, const int32_t* inds_c, const int32_t* dims, int32_t n_dims,
+                     int32_t path, void* stream);
+
+/* number of kernel launches this library issued since load (evidence counter) */
+int64_t tn_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_H_ */

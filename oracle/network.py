@@ -115,7 +115,8 @@ def build_network(circ, diag_hyper: bool = False, eps_frac: float = 0.01) -> Net
         fcount[a] += 1
         fcount[b] += 1
         xa, xb = pos[a], pos[b]
-        ltab = max(ltab, math.sqrt((xa[0] - xb[0]) ** 2 + (xa[1] - xb[1]) ** 2))
+        dx, dy = float(xa[0] - xb[0]), float(xa[1] - xb[1])
+        ltab = max(ltab, math.sqrt(dx * dx + dy * dy))
         pa = (float(xa[0] + (xb[0] - xa[0]) / 4.0), float(xa[1] + (xb[1] - xa[1]) / 4.0))
         pb = (float(xb[0] + (xa[0] - xb[0]) / 4.0), float(xb[1] + (xa[1] - xb[1]) / 4.0))
         diag = _is_diag(U)
@@ -213,13 +214,15 @@ def build_network(circ, diag_hyper: bool = False, eps_frac: float = 0.01) -> Net
     rmin = math.inf
     for i in range(n):
         for j in range(i + 1, n):
-            d = math.sqrt((pos[i, 0] - pos[j, 0]) ** 2 + (pos[i, 1] - pos[j, 1]) ** 2)
+            dx, dy = float(pos[i, 0] - pos[j, 0]), float(pos[i, 1] - pos[j, 1])
+            d = math.sqrt(dx * dx + dy * dy)
             rmin = min(rmin, d)
     if not math.isfinite(rmin) or rmin <= 0:
         rmin = 1.0
     radius = ltab / 4.0 + eps_frac * rmin
     F = max(fcount) if fcount else 0
     # k bound: only U (no U^dagger) -> F ((l/4 + r/4)/(r/4))^d, d = 2 (l.123)
-    k_bound = max(1.0, F * ((ltab + rmin) / rmin) ** 2)
+    g = (ltab + rmin) / rmin
+    k_bound = max(1.0, float(F) * (g * g))
     return Network(dims, final, out_leg, out_owner, radius, k_bound, n,
                    extras=dict(l=ltab, r=rmin, F=F, diag_hyper=diag_hyper))

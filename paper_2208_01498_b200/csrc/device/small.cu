@@ -1,0 +1,90 @@
+// Small-tensor path: many independent early-stage pairwise contractions (bond
+// dimensions 2-16, a few to a few thousand entries) batched into ONE launch per
+// wave of the contraction tree.  HBM/latency bound, so it runs on the CUDA cores:
+// each thread owns output elements, the permutation to matricised form is folded
+// into the loads through the GroupMap offset tables (no transpose pass).
+// PAPER.md Fig. 1b (l.54): C = sum over shared indices of A * B.
+#include "common.cuh"
+
+namespace tnd {
+
+template <typename R>
+__global__ void __launch_bounds__(128) small_contract_kernel(
+    const SmallStep* __restrict__ steps, const int64_t* __restrict__ cta_prefix, int32_t n_steps,
+    const int64_t* __restrict__ tab, void* const* __restrict__ ptrs, int32_t outs_per_cta) {
+  using C2 = typename cplx_t<R>::type;
+  // step of this CTA: last s with cta_prefix[s] <= blockIdx.x
+  int lo = 0, hi = n_steps - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(cta_prefix + mid) <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const SmallStep& d = steps[lo];
+  const C2* __restrict__ A = reinterpret_cast<const C2*>(ptrs[d.a]);
+  const C2* __restrict__ B = reinterpret_cast<const C2*>(ptrs[d.b]);
+  C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[d.c]);
+  const int64_t start = ((int64_t)blockIdx.x - cta_prefix[lo]) * outs_per_cta;
+  const int64_t total = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
+  const int64_t end = min(total, start + outs_per_cta);
+  const int64_t K = int64_t(1) << d.k_bits;
+  const int64_t nmask = (int64_t(1) << d.n_bits) - 1, mmask = (int64_t(1) << d.m_bits) - 1;
+  for (int64_t o = start + threadIdx.x; o < end; o += blockDim.x) {
+    const int64_t n = o & nmask;
+    const int64_t m = (o >> d.n_bits) & mmask;
+    const int64_t bb = o >> (d.n_bits + d.m_bits);
+    const int64_t ao = gmap(tab, d.Ab, bb) + gmap(tab, d.Am, m);
+    const int64_t bo = gmap(tab, d.Bb, bb) + gmap(tab, d.Bn, n);
+    R re = 0, im = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      const C2 a = A[ao + gmap(tab, d.Ak, k)];
+      const C2 b = B[bo + gmap(tab, d.Bk, k)];
+      re = fma(a.x, b.x, re);
+      re = fma(-a.y, b.y, re);
+      im = fma(a.x, b.y, im);
+      im = fma(a.y, b.x, im);
+    }
+    C[o] = C2{re, im};
+  }
+}
+
+// Leaf pointers of one (bitstring, slice) pass: a leaf whose output legs / sliced
+// indices are bound to values v_j lives at base + sum_j v_j * stride_j.
+// var_kind >= 0: qubit id (value = bits[q]); var_kind < 0: sliced index number
+// (-1 - j), value = digit j of the slice id (last sliced index fastest).
+__global__ void set_leaf_ptrs_kernel(void** __restrict__ ptrs, const int64_t* __restrict__ leaf_base,
+                                     const int32_t* __restrict__ var_begin, const int32_t* __restrict__ var_kind,
+                                     const int64_t* __restrict__ var_stride, int32_t n_leaves,
+                                     const uint8_t* __restrict__ bits, const int64_t* __restrict__ slice_id,
+                                     const int32_t* __restrict__ slice_dim_log2, const int32_t* __restrict__ slice_shift,
+                                     int32_t elem_bytes, char* arena_leaves) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_leaves) return;
+  int64_t off = leaf_base[t];
+  const int64_t s = *slice_id;
+  for (int v = var_begin[t]; v < var_begin[t + 1]; ++v) {
+    int k = var_kind[v];
+    int64_t val;
+    if (k >= 0) val = bits[k];
+    else {
+      int j = -1 - k;
+      val = (s >> slice_shift[j]) & ((int64_t(1) << slice_dim_log2[j]) - 1);
+    }
+    off += val * var_stride[v];
+  }
+  ptrs[t] = arena_leaves + off * elem_bytes;
+}
+
+// amp += root scalar; advance the slice counter (one thread)
+template <typename R>
+__global__ void accumulate_root_kernel(const void* const* __restrict__ ptrs, int32_t root,
+                                       void* __restrict__ amp, int64_t* __restrict__ slice_id) {
+  using C2 = typename cplx_t<R>::type;
+  const C2 v = *reinterpret_cast<const C2*>(ptrs[root]);
+  C2* a = reinterpret_cast<C2*>(amp);
+  a->x += v.x;
+  a->y += v.y;
+  *slice_id += 1;
+}
+
+
+}  // namespace tnd

@@ -1,0 +1,1085 @@
+// Runtime of the B200 contraction engine: C-ABI (include/tn.h), execution plans,
+// device arena, launch schedule and CUDA-graph replay.
+//
+// A plan turns (network, order) into:
+//   * leaf tensors resident in HBM, output legs and sliced indices moved to the
+//     front so that binding a bitstring / slice is a pointer offset (no copies);
+//   * for every pairwise step of the order (Eq. (3)), its index classes
+//     (batch / left / right / contracted) and a kernel path: the warp-batched small
+//     kernel (one launch per wave of independent steps) or the tcgen05 GEMM
+//     (pack + GEMM) for GEMM-shaped complex64 steps;
+//   * one device arena: every intermediate and every pack buffer gets an offset by
+//     first-fit over its live interval in the launch sequence (memory planner);
+//   * one CUDA graph per slice, replayed for every slice and bitstring.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device/common.cuh"
+#include "device/gemm_tc.cu"
+#include "device/small.cu"
+#include "host/tn_host.hpp"
+#include "tn.h"
+
+using tnd::GroupMap;
+using tnd::PackDesc;
+using tnd::SmallStep;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct Err : std::runtime_error {
+  int code;
+  Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define CK(x)                                                                                         \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) throw Err(TN_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TN_OK;
+  } catch (const Err& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TN_EINTERNAL;
+  }
+}
+
+constexpr int OUTS_PER_CTA = 512;
+constexpr int64_t ALIGN = 1024;
+
+// ------------------------------------------------------------- table pool ---
+struct TabPool {
+  std::vector<int64_t> v;
+  // dims: (log2 dim, element stride) of the group's indices in group order (last fastest)
+  GroupMap add(const std::vector<std::pair<int, int64_t>>& g) {
+    int bits = 0;
+    for (auto& p : g) bits += p.first;
+    GroupMap m;
+    m.bits = bits;
+    m.lo_bits = bits - bits / 2;
+    auto off = [&](int64_t x) {
+      int64_t o = 0;
+      int sh = 0;
+      for (int i = (int)g.size() - 1; i >= 0; --i) {
+        o += ((x >> sh) & ((int64_t(1) << g[i].first) - 1)) * g[i].second;
+        sh += g[i].first;
+      }
+      return o;
+    };
+    m.lo_off = (int64_t)v.size();
+    for (int64_t x = 0; x < (int64_t(1) << m.lo_bits); ++x) v.push_back(off(x));
+    m.hi_off = (int64_t)v.size();
+    for (int64_t y = 0; y < (int64_t(1) << (bits - m.lo_bits)); ++y) v.push_back(off(y << m.lo_bits));
+    return m;
+  }
+};
+
+struct NodeLayout {
+  std::vector<int> inds;  // stored order (row-major)
+  int bits = 0;
+};
+
+std::vector<std::pair<int, int64_t>> group_of(const std::vector<int>& group, const NodeLayout& L,
+                                              const std::vector<int>& l2) {
+  // element strides of L's stored layout
+  std::vector<int64_t> st(L.inds.size());
+  int64_t acc = 1;
+  for (int k = (int)L.inds.size() - 1; k >= 0; --k) {
+    st[k] = acc;
+    acc <<= l2[L.inds[k]];
+  }
+  std::vector<std::pair<int, int64_t>> g;
+  for (int i : group) {
+    auto it = std::find(L.inds.begin(), L.inds.end(), i);
+    if (it == L.inds.end()) throw Err(TN_EINTERNAL, "index not in operand");
+    g.push_back({l2[i], st[it - L.inds.begin()]});
+  }
+  return g;
+}
+
+// index classes of a pairwise step
+struct Classes {
+  std::vector<int> batch, lfree, rfree, contr;
+};
+Classes classify(const NodeLayout& A, const NodeLayout& B, const std::set<int>& kept) {
+  Classes c;
+  std::set<int> sb(B.inds.begin(), B.inds.end()), sa(A.inds.begin(), A.inds.end());
+  for (int i : A.inds) {
+    if (sb.count(i)) (kept.count(i) ? c.batch : c.contr).push_back(i);
+    else {
+      if (!kept.count(i)) throw Err(TN_EUNSUPPORTED, "index private to one operand must be kept");
+      c.lfree.push_back(i);
+    }
+  }
+  for (int i : B.inds)
+    if (!sa.count(i)) {
+      if (!kept.count(i)) throw Err(TN_EUNSUPPORTED, "index private to one operand must be kept");
+      c.rfree.push_back(i);
+    }
+  return c;
+}
+int sum_bits(const std::vector<int>& g, const std::vector<int>& l2) {
+  int b = 0;
+  for (int i : g) b += l2[i];
+  return b;
+}
+
+// ---------------------------------------------------------- tensor maps -----
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Err(TN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cuuint64_t(1) << k_bits, cuuint64_t(1) << r_bits, cuuint64_t(6) << nb_bits};
+  cuuint64_t strides[2] = {(cuuint64_t(1) << k_bits) * 2, (cuuint64_t(1) << (k_bits + r_bits)) * 2};
+  cuuint32_t box[3] = {(cuuint32_t)tnd::tc::BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(TN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+template <int BN>
+void ensure_gemm_attr() {
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(tnd::tc::cgemm_bf16x6_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            tnd::tc::Cfg<BN>::SMEM));
+    done = true;
+  }
+}
+
+// one tensor-core step: pack X, pack Y, GEMM
+struct TcStep {
+  PackDesc px, py;
+  int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
+  int32_t c_node;
+  int nb_bits, m_bits, n_bits, k_bits, BN;
+  CUtensorMap ta, tb;
+  double flops;
+};
+
+void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
+               cudaEvent_t ev_mid = nullptr) {
+  auto pack = [&](const PackDesc& d, int64_t off, int r_bits) {
+    const int64_t nvec = (int64_t(1) << (d.nb_bits + r_bits + d.k_bits)) >> 3;
+    const int64_t blocks = std::min<int64_t>((nvec + 255) / 256, 148 * 64);
+    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, 256, 0, st>>>(ptrs_d, d, tab_d,
+                                                              reinterpret_cast<__nv_bfloat16*>(arena + off));
+    g_launches++;
+  };
+  pack(t.px, t.x_off, t.m_bits);
+  pack(t.py, t.y_off, t.n_bits);
+  if (ev_mid) CK(cudaEventRecord(ev_mid, st));
+  dim3 grid((unsigned)(((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN), (unsigned)(((int64_t(1) << t.m_bits) + 127) / 128),
+            (unsigned)(1u << t.nb_bits));
+  if (t.BN == 128) {
+    ensure_gemm_attr<128>();
+    tnd::tc::cgemm_bf16x6_kernel<128><<<grid, 128, tnd::tc::Cfg<128>::SMEM, st>>>(
+        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, 0);
+  } else {
+    ensure_gemm_attr<64>();
+    tnd::tc::cgemm_bf16x6_kernel<64><<<grid, 128, tnd::tc::Cfg<64>::SMEM, st>>>(
+        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, 0);
+  }
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+struct Wave {
+  double flops = 0, bytes = 0;
+  std::vector<SmallStep> steps;
+  std::vector<int64_t> prefix;
+  SmallStep* steps_d = nullptr;
+  int64_t* prefix_d = nullptr;
+  int64_t n_cta = 0;
+};
+
+template <typename R>
+void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st) {
+  tnd::small_contract_kernel<R><<<(unsigned)w.n_cta, 128, 0, st>>>(w.steps_d, w.prefix_d, (int)w.steps.size(), tab_d,
+                                                                     ptrs_d, OUTS_PER_CTA);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+// decide the path of a step (TC only for complex64 GEMM-shaped steps)
+bool want_tc(int dtype, int nb, int m, int n, int k) {
+  if (dtype != TN_C64) return false;
+  return k >= 4 && std::max(m, n) >= 6 && std::min(m, n) >= 4 && (nb + m + n + k) >= 22;
+}
+
+// first-fit offsets for (size, [lo, hi]) items
+std::vector<int64_t> first_fit(const std::vector<int64_t>& size, const std::vector<std::pair<int, int>>& iv,
+                               int64_t& total) {
+  size_t n = size.size();
+  std::vector<size_t> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return size[a] > size[b]; });
+  std::vector<int64_t> off(n, -1);
+  std::vector<size_t> placed;
+  total = 0;
+  for (size_t it : ord) {
+    int64_t sz = (size[it] + ALIGN - 1) / ALIGN * ALIGN;
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (size_t p : placed)
+      if (!(iv[p].second < iv[it].first || iv[it].second < iv[p].first))
+        busy.push_back({off[p], off[p] + (size[p] + ALIGN - 1) / ALIGN * ALIGN});
+    std::sort(busy.begin(), busy.end());
+    int64_t o = 0;
+    for (auto& b : busy) {
+      if (o + sz <= b.first) break;
+      o = std::max(o, b.second);
+    }
+    off[it] = o;
+    placed.push_back(it);
+    total = std::max(total, o + sz);
+  }
+  return off;
+}
+
+}  // namespace
+
+// =============================================================== handles ======
+struct tn_network_s {
+  tn::Network net;
+};
+struct tn_order_s {
+  tn::Order ord;
+  const tn::Network* net;
+};
+
+struct tn_plan_s {
+  const tn::Network* net = nullptr;
+  int dtype = TN_C64, device = 0, esz = 8;
+  int n_leaves = 0, n_nodes = 0, root = 0;
+  std::vector<int> l2;
+  std::vector<Wave> waves;
+  std::vector<TcStep> tcs;
+  std::vector<std::pair<int, int>> launches;  // (0, wave) | (1, tc)
+  int64_t n_slices = 1;
+  double flops = 0, tc_flops = 0;
+  int n_small = 0;
+  // device
+  char* arena = nullptr;
+  int64_t arena_bytes = 0;
+  char* leaves = nullptr;
+  int64_t* tab_d = nullptr;
+  void** ptrs_d = nullptr;
+  int64_t* leaf_base_d = nullptr;
+  int32_t* var_begin_d = nullptr;
+  int32_t* var_kind_d = nullptr;
+  int64_t* var_stride_d = nullptr;
+  int32_t* sl_log2_d = nullptr;
+  int32_t* sl_shift_d = nullptr;
+  uint8_t* bits_d = nullptr;
+  int64_t* slice_d = nullptr;
+  void* amp_d = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t kernels_per_slice = 0;
+  std::vector<int32_t> step_table;   // 6 per step: path, nb, m, n, k, launch position
+
+  void record(cudaStream_t st) {
+    tnd::set_leaf_ptrs_kernel<<<(n_leaves + 127) / 128, 128, 0, st>>>(
+        ptrs_d, leaf_base_d, var_begin_d, var_kind_d, var_stride_d, n_leaves, bits_d, slice_d, sl_log2_d, sl_shift_d,
+        esz, leaves);
+    int64_t k = 1;
+    for (auto& L : launches) {
+      if (L.first == 0) {
+        if (dtype == TN_C64) launch_wave<float>(waves[L.second], ptrs_d, tab_d, st);
+        else launch_wave<double>(waves[L.second], ptrs_d, tab_d, st);
+        k += 1;
+      } else {
+        launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
+        k += 3;
+      }
+    }
+    if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
+    CK(cudaGetLastError());
+    kernels_per_slice = k + 1;
+  }
+
+  ~tn_plan_s() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (cap) cudaStreamDestroy(cap);
+    for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
+    for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
+                    (void*)var_kind_d, (void*)var_stride_d, (void*)sl_log2_d, (void*)sl_shift_d, (void*)bits_d,
+                    (void*)slice_d, amp_d})
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+__global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
+template <typename R>
+__global__ void add_amp_kernel(void* dst, const void* src) {
+  using C2 = typename tnd::cplx_t<R>::type;
+  C2* d = reinterpret_cast<C2*>(dst);
+  const C2* s = reinterpret_cast<const C2*>(src);
+  d->x += s->x;
+  d->y += s->y;
+}
+
+template <typename T>
+T* upload(const std::vector<T>& v) {
+  T* p = nullptr;
+  size_t n = std::max<size_t>(v.size(), 1);
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+void check_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0)
+    throw Err(TN_ECUDA, "no CUDA device " + std::to_string(device));
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, device));
+  if (p.major != 10) throw Err(TN_ECUDA, std::string("sm_100 device required, found ") + p.name);
+  CK(cudaSetDevice(device));
+}
+
+void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
+  P.net = &net;
+  P.esz = P.dtype == TN_C64 ? 8 : 16;
+  const int n = (int)net.tensors.size();
+  P.n_leaves = n;
+  P.n_nodes = n + (int)ord.steps.size();
+  P.root = P.n_nodes - 1;
+  P.l2.resize(net.dims.size());
+  for (size_t i = 0; i < net.dims.size(); ++i) P.l2[i] = net.log2dim((int)i);
+  const auto& l2 = P.l2;
+  std::set<int> sliced(ord.slices.begin(), ord.slices.end());
+  std::map<int, int> slice_pos;
+  for (size_t j = 0; j < ord.slices.size(); ++j) slice_pos[ord.slices[j]] = (int)j;
+  std::map<int, int> out_q;
+  for (int q = 0; q < net.n_qubits; ++q) out_q[net.out_leg[q]] = q;
+
+  // ---- leaves: vars (output legs, sliced indices) first ----
+  std::vector<NodeLayout> L(P.n_nodes);
+  std::vector<int64_t> leaf_base(n), var_stride;
+  std::vector<int32_t> var_begin(n + 1, 0), var_kind;
+  std::vector<char> leaf_host;
+  int64_t leaf_elems = 0;
+  for (int t = 0; t < n; ++t) {
+    const auto& T = net.tensors[t];
+    std::vector<int> vars, rest;
+    for (int i : T.inds) (out_q.count(i) || sliced.count(i) ? vars : rest).push_back(i);
+    L[t].inds = rest;
+    L[t].bits = sum_bits(rest, l2);
+    std::vector<int> ninds = vars;
+    ninds.insert(ninds.end(), rest.begin(), rest.end());
+    // strides of the original (canonical) layout
+    std::vector<int64_t> st(T.inds.size());
+    int64_t acc = 1;
+    for (int k = (int)T.inds.size() - 1; k >= 0; --k) { st[k] = acc; acc *= net.dims[T.inds[k]]; }
+    leaf_base[t] = leaf_elems;
+    var_begin[t] = (int32_t)var_kind.size();
+    int64_t vs = int64_t(1) << L[t].bits;
+    std::vector<int64_t> vstr(vars.size());
+    for (int k = (int)vars.size() - 1; k >= 0; --k) { vstr[k] = vs; vs <<= l2[vars[k]]; }
+    for (size_t k = 0; k < vars.size(); ++k) {
+      var_kind.push_back(out_q.count(vars[k]) ? out_q[vars[k]] : -1 - slice_pos[vars[k]]);
+      var_stride.push_back(vstr[k]);
+    }
+    var_begin[t + 1] = (int32_t)var_kind.size();
+    // permuted data
+    size_t off = leaf_host.size();
+    leaf_host.resize(off + (size_t)acc * P.esz);
+    std::vector<int> dig(ninds.size());
+    for (int64_t it = 0; it < acc; ++it) {
+      int64_t r = it;
+      for (int k = (int)ninds.size() - 1; k >= 0; --k) { dig[k] = (int)(r % net.dims[ninds[k]]); r /= net.dims[ninds[k]]; }
+      int64_t src = 0;
+      for (size_t k = 0; k < ninds.size(); ++k) {
+        size_t pos = std::find(T.inds.begin(), T.inds.end(), ninds[k]) - T.inds.begin();
+        src += st[pos] * dig[k];
+      }
+      const tn::cplx z = T.data[src];
+      if (P.dtype == TN_C64) {
+        float v[2] = {(float)z.real(), (float)z.imag()};
+        std::memcpy(&leaf_host[off + it * 8], v, 8);
+      } else {
+        double v[2] = {z.real(), z.imag()};
+        std::memcpy(&leaf_host[off + it * 16], v, 16);
+      }
+    }
+    leaf_elems += acc;
+    // keep leaf bases 128-byte aligned
+    int64_t pad = (16 - (leaf_elems % 16)) % 16;
+    leaf_elems += pad;
+    leaf_host.resize((size_t)leaf_elems * P.esz, 0);
+  }
+
+  // ---- steps ----
+  auto kept_all = tn::kept_per_step(net, ord.steps);
+  std::vector<int> parent(P.n_nodes, -1);
+  std::vector<int> kind(ord.steps.size(), 0), big_index(ord.steps.size(), -1);
+  TabPool pool;
+  std::vector<SmallStep> small_desc(ord.steps.size());
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    int a = ord.steps[k].first, b = ord.steps[k].second, c = n + (int)k;
+    parent[a] = parent[b] = (int)k;
+    std::set<int> kept;
+    for (int i : kept_all[k]) if (!sliced.count(i)) kept.insert(i);
+    Classes cl = classify(L[a], L[b], kept);
+    int nb = sum_bits(cl.batch, l2), ml = sum_bits(cl.lfree, l2), mr = sum_bits(cl.rfree, l2), kk = sum_bits(cl.contr, l2);
+    P.flops += 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
+    if (want_tc(P.dtype, nb, ml, mr, kk)) {
+      // X = operand with the larger free group becomes the MMA's M side
+      bool swap = mr > ml;
+      int X = swap ? b : a, Y = swap ? a : b;
+      const auto& fx = swap ? cl.rfree : cl.lfree;
+      const auto& fy = swap ? cl.lfree : cl.rfree;
+      TcStep t;
+      t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
+      t.BN = (t.n_bits >= 7) ? 128 : 64;
+      t.c_node = c;
+      t.px.src = X; t.px.nb_bits = nb; t.px.r_bits = t.m_bits; t.px.k_bits = kk;
+      t.px.gb = pool.add(group_of(cl.batch, L[X], l2));
+      t.px.gr = pool.add(group_of(fx, L[X], l2));
+      t.px.gk = pool.add(group_of(cl.contr, L[X], l2));
+      t.py.src = Y; t.py.nb_bits = nb; t.py.r_bits = t.n_bits; t.py.k_bits = kk;
+      t.py.gb = pool.add(group_of(cl.batch, L[Y], l2));
+      t.py.gr = pool.add(group_of(fy, L[Y], l2));
+      t.py.gk = pool.add(group_of(cl.contr, L[Y], l2));
+      t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
+      P.tc_flops += t.flops;
+      L[c].inds = cl.batch;
+      L[c].inds.insert(L[c].inds.end(), fx.begin(), fx.end());
+      L[c].inds.insert(L[c].inds.end(), fy.begin(), fy.end());
+      kind[k] = 1;
+      big_index[k] = (int)P.tcs.size();
+      P.tcs.push_back(t);
+    } else {
+      SmallStep d{};
+      d.a = a; d.b = b; d.c = c;
+      d.nb_bits = nb; d.m_bits = ml; d.n_bits = mr; d.k_bits = kk;
+      d.Ab = pool.add(group_of(cl.batch, L[a], l2));
+      d.Am = pool.add(group_of(cl.lfree, L[a], l2));
+      d.Ak = pool.add(group_of(cl.contr, L[a], l2));
+      d.Bb = pool.add(group_of(cl.batch, L[b], l2));
+      d.Bk = pool.add(group_of(cl.contr, L[b], l2));
+      d.Bn = pool.add(group_of(cl.rfree, L[b], l2));
+      small_desc[k] = d;
+      L[c].inds = cl.batch;
+      L[c].inds.insert(L[c].inds.end(), cl.lfree.begin(), cl.lfree.end());
+      L[c].inds.insert(L[c].inds.end(), cl.rfree.begin(), cl.rfree.end());
+      P.n_small++;
+    }
+    L[c].bits = sum_bits(L[c].inds, l2);
+  }
+
+  P.step_table.assign(6 * ord.steps.size(), 0);
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    int32_t* e = &P.step_table[6 * k];
+    if (kind[k]) {
+      const auto& t = P.tcs[big_index[k]];
+      e[0] = TN_PATH_TC; e[1] = t.nb_bits; e[2] = t.m_bits; e[3] = t.n_bits; e[4] = t.k_bits;
+    } else {
+      const auto& d = small_desc[k];
+      e[0] = TN_PATH_SMALL; e[1] = d.nb_bits; e[2] = d.m_bits; e[3] = d.n_bits; e[4] = d.k_bits;
+    }
+  }
+  // ---- schedule: small steps in waves between tensor-core steps ----
+  std::vector<int> slot(ord.steps.size(), 0), depth(ord.steps.size(), 0);
+  int n_big = (int)P.tcs.size();
+  std::vector<std::map<int, std::vector<int>>> slot_waves(n_big + 1);
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    if (kind[k]) continue;
+    int s = 0;
+    for (int ch : {ord.steps[k].first, ord.steps[k].second}) {
+      if (ch < n) continue;
+      int ck = ch - n;
+      s = std::max(s, kind[ck] ? big_index[ck] + 1 : slot[ck]);
+    }
+    int d = 1;
+    for (int ch : {ord.steps[k].first, ord.steps[k].second}) {
+      if (ch < n) continue;
+      int ck = ch - n;
+      if (!kind[ck] && slot[ck] == s) d = std::max(d, depth[ck] + 1);
+    }
+    slot[k] = s;
+    depth[k] = d;
+    slot_waves[s][d].push_back((int)k);
+  }
+  std::vector<int> step_pos(ord.steps.size(), 0);
+  for (int s = 0; s <= n_big; ++s) {
+    for (auto& kv : slot_waves[s]) {
+      Wave w;
+      int64_t acc = 0;
+      for (int k : kv.second) {
+        w.prefix.push_back(acc);
+        const auto& d = small_desc[k];
+        int64_t outs = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
+        acc += (outs + OUTS_PER_CTA - 1) / OUTS_PER_CTA;
+        w.steps.push_back(d);
+        w.flops += 8.0 * std::ldexp(1.0, d.nb_bits + d.m_bits + d.n_bits + d.k_bits);
+        w.bytes += P.esz * (std::ldexp(1.0, L[d.a].bits) + std::ldexp(1.0, L[d.b].bits) + std::ldexp(1.0, L[d.c].bits));
+        step_pos[k] = (int)P.launches.size();
+      }
+      w.prefix.push_back(acc);
+      w.n_cta = acc;
+      P.launches.push_back({0, (int)P.waves.size()});
+      P.waves.push_back(std::move(w));
+    }
+    if (s < n_big) {
+      for (size_t k = 0; k < ord.steps.size(); ++k)
+        if (kind[k] && big_index[k] == s) step_pos[k] = (int)P.launches.size();
+      P.launches.push_back({1, s});
+    }
+  }
+
+  for (size_t k = 0; k < ord.steps.size(); ++k) P.step_table[6 * k + 5] = step_pos[k];
+  // ---- arena: intermediates + pack buffers, first fit over live intervals ----
+  std::vector<int64_t> sizes;
+  std::vector<std::pair<int, int>> ivs;
+  std::vector<int> owner;  // >=0: node id; -1 - 2*tc: pack X; -2 - 2*tc: pack Y
+  const int last = (int)P.launches.size();
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    int c = n + (int)k;
+    int hi = parent[c] >= 0 ? step_pos[parent[c]] : last;
+    sizes.push_back((int64_t(1) << L[c].bits) * P.esz);
+    ivs.push_back({step_pos[k], hi});
+    owner.push_back(c);
+  }
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    if (!kind[k]) continue;
+    const auto& t = P.tcs[big_index[k]];
+    sizes.push_back((int64_t(12) << (t.nb_bits + t.m_bits + t.k_bits)));
+    ivs.push_back({step_pos[k], step_pos[k]});
+    owner.push_back(-1 - 2 * big_index[k]);
+    sizes.push_back((int64_t(12) << (t.nb_bits + t.n_bits + t.k_bits)));
+    ivs.push_back({step_pos[k], step_pos[k]});
+    owner.push_back(-2 - 2 * big_index[k]);
+  }
+  int64_t total = 0;
+  auto offs = first_fit(sizes, ivs, total);
+  P.arena_bytes = std::max<int64_t>(total, ALIGN);
+  size_t free_b = 0, tot_b = 0;
+  CK(cudaMemGetInfo(&free_b, &tot_b));
+  if ((size_t)P.arena_bytes + (size_t)(leaf_host.size() + pool.v.size() * 8) + (size_t(1) << 30) > free_b)
+    throw Err(TN_ENOMEM, "arena of " + std::to_string(P.arena_bytes) + " bytes does not fit free device memory " +
+                             std::to_string(free_b));
+  CK(cudaMalloc(&P.arena, P.arena_bytes));
+  std::vector<void*> ptrs(P.n_nodes, nullptr);
+  for (size_t j = 0; j < owner.size(); ++j) {
+    if (owner[j] >= 0) ptrs[owner[j]] = P.arena + offs[j];
+    else {
+      int o = -1 - owner[j];
+      if (o % 2 == 0) P.tcs[o / 2].x_off = offs[j];
+      else P.tcs[o / 2].y_off = offs[j];
+    }
+  }
+  for (auto& t : P.tcs) {
+    t.ta = make_plane_map(P.arena + t.x_off, t.k_bits, t.m_bits, t.nb_bits, 128);
+    t.tb = make_plane_map(P.arena + t.y_off, t.k_bits, t.n_bits, t.nb_bits, t.BN);
+  }
+
+  // ---- uploads ----
+  P.leaves = upload(leaf_host);
+  P.tab_d = upload(pool.v);
+  P.ptrs_d = upload(ptrs);
+  P.leaf_base_d = upload(leaf_base);
+  P.var_begin_d = upload(var_begin);
+  P.var_kind_d = upload(var_kind);
+  P.var_stride_d = upload(var_stride);
+  std::vector<int32_t> sl_log2, sl_shift(ord.slices.size());
+  int sh = 0;
+  for (int j = (int)ord.slices.size() - 1; j >= 0; --j) { sl_shift[j] = sh; sh += l2[ord.slices[j]]; }
+  for (int i : ord.slices) sl_log2.push_back(l2[i]);
+  P.n_slices = int64_t(1) << sh;
+  P.sl_log2_d = upload(sl_log2);
+  P.sl_shift_d = upload(sl_shift);
+  CK(cudaMalloc(&P.bits_d, std::max(1, net.n_qubits)));
+  CK(cudaMemset(P.bits_d, 0, std::max(1, net.n_qubits)));
+  CK(cudaMalloc(&P.slice_d, sizeof(int64_t)));
+  CK(cudaMemset(P.slice_d, 0, sizeof(int64_t)));
+  CK(cudaMalloc(&P.amp_d, 16));
+  CK(cudaMemset(P.amp_d, 0, 16));
+  for (auto& w : P.waves) {
+    w.steps_d = upload(w.steps);
+    w.prefix_d = upload(w.prefix);
+  }
+  if (n == 1 && ord.steps.empty()) P.root = 0;
+  // ---- capture one slice as a CUDA graph ----
+  ensure_gemm_attr<128>();
+  ensure_gemm_attr<64>();
+  CK(cudaStreamCreateWithFlags(&P.cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(P.cap, cudaStreamCaptureModeThreadLocal));
+  int64_t before = g_launches.load();
+  P.record(P.cap);
+  g_launches = before;  // captured launches are counted when replayed
+  CK(cudaStreamEndCapture(P.cap, &g));
+  CK(cudaGraphInstantiate(&P.graph, g, 0));
+  CK(cudaGraphDestroy(g));
+}
+
+void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_profile& pr) {
+  std::memset(&pr, 0, sizeof(pr));
+  const size_t nl = P.launches.size();
+  std::vector<cudaEvent_t> ev(2 * nl + 4);
+  std::vector<cudaEvent_t> mid(nl, nullptr);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  for (size_t j = 0; j < nl; ++j)
+    if (P.launches[j].first == 1) CK(cudaEventCreate(&mid[j]));
+  for (int64_t s = s0; s < s1; ++s) {
+    CK(cudaEventRecord(ev[0], st));
+    tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
+        P.ptrs_d, P.leaf_base_d, P.var_begin_d, P.var_kind_d, P.var_stride_d, P.n_leaves, P.bits_d, P.slice_d,
+        P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
+    g_launches++;
+    CK(cudaEventRecord(ev[1], st));
+    for (size_t j = 0; j < nl; ++j) {
+      const auto& L = P.launches[j];
+      CK(cudaEventRecord(ev[2 + 2 * j], st));
+      if (L.first == 0) {
+        if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
+        else launch_wave<double>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
+      } else {
+        launch_tc(P.tcs[L.second], P.arena, P.ptrs_d, P.tab_d, st, mid[j]);
+      }
+      CK(cudaEventRecord(ev[3 + 2 * j], st));
+    }
+    CK(cudaEventRecord(ev[2 + 2 * nl], st));
+    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
+    g_launches++;
+    CK(cudaEventRecord(ev[3 + 2 * nl], st));
+    CK(cudaEventSynchronize(ev[3 + 2 * nl]));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    pr.ms_other += ms;
+    CK(cudaEventElapsedTime(&ms, ev[2 + 2 * nl], ev[3 + 2 * nl]));
+    pr.ms_other += ms;
+    pr.n_other += 2;
+    for (size_t j = 0; j < nl; ++j) {
+      const auto& L = P.launches[j];
+      if (L.first == 0) {
+        CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
+        pr.ms_small += ms;
+        pr.n_small += 1;
+        pr.flops_small += P.waves[L.second].flops;
+        pr.bytes_small += P.waves[L.second].bytes;
+      } else {
+        const auto& t = P.tcs[L.second];
+        CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], mid[j]));
+        pr.ms_pack += ms;
+        CK(cudaEventElapsedTime(&ms, mid[j], ev[3 + 2 * j]));
+        pr.ms_gemm += ms;
+        pr.n_pack += 2;
+        pr.n_gemm += 1;
+        pr.flops_gemm += t.flops;
+        pr.bytes_pack += (double)P.esz * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
+                                          std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits)) * 2.5;  // read 8 B, write 12 B
+      }
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& e : mid) if (e) cudaEventDestroy(e);
+}
+
+void run_slices(tn_plan_s& P, const uint8_t* bits, bool bits_on_device, int64_t s0, int64_t s1, cudaStream_t st) {
+  if (s0 < 0 || s1 > P.n_slices || s0 > s1) throw Err(TN_EINVAL, "slice range out of bounds");
+  CK(cudaSetDevice(P.device));
+  if (P.net->n_qubits > 0)
+    CK(cudaMemcpyAsync(P.bits_d, bits, P.net->n_qubits, bits_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  set_i64_kernel<<<1, 1, 0, st>>>(P.slice_d, s0);
+  CK(cudaMemsetAsync(P.amp_d, 0, 16, st));
+  for (int64_t s = s0; s < s1; ++s) {
+    CK(cudaGraphLaunch(P.graph, st));
+    g_launches += P.kernels_per_slice;
+  }
+}
+
+}  // namespace
+
+// ================================================================== C ABI =====
+extern "C" {
+
+const char* tn_last_error(void) { return g_err.c_str(); }
+const char* tn_version(void) { return "paper_2208_01498_b200 0.1 (sm_100a)"; }
+int64_t tn_kernel_launches(void) { return g_launches.load(); }
+
+int tn_build_network(int32_t n_qubits, const double* qubit_xy, int32_t n_gates, const int32_t* gate_qubits,
+                     const double* gate_mats, int32_t diag_hyper, tn_network* out) {
+  return guard([&] {
+    if (!out || n_qubits < 1 || !qubit_xy || n_gates < 0 || (n_gates > 0 && (!gate_qubits || !gate_mats)))
+      throw Err(TN_EINVAL, "tn_build_network: bad arguments");
+    for (int g = 0; g < n_gates; ++g) {
+      int a = gate_qubits[2 * g], b = gate_qubits[2 * g + 1];
+      if (a < 0 || a >= n_qubits || b >= n_qubits || b == a || b < -1)
+        throw Err(TN_EINVAL, "tn_build_network: bad qubit ids in gate " + std::to_string(g));
+    }
+    auto h = std::make_unique<tn_network_s>();
+    h->net = tn::build_network(n_qubits, qubit_xy, n_gates, gate_qubits, gate_mats, diag_hyper != 0);
+    *out = h.release();
+  });
+}
+void tn_network_free(tn_network net) { delete net; }
+
+int tn_network_get_info(tn_network h, tn_network_info* info) {
+  return guard([&] {
+    if (!h || !info) throw Err(TN_EINVAL, "null");
+    info->n_tensors = (int32_t)h->net.tensors.size();
+    info->n_indices = (int32_t)h->net.dims.size();
+    info->n_qubits = h->net.n_qubits;
+    int mr = 0;
+    for (auto& t : h->net.tensors) mr = std::max(mr, (int)t.inds.size());
+    info->max_rank = mr;
+    info->radius = h->net.radius;
+    info->k_bound = h->net.k_bound;
+  });
+}
+int tn_network_dims(tn_network h, int32_t* dims, int32_t* out_legs) {
+  return guard([&] {
+    if (!h) throw Err(TN_EINVAL, "null");
+    if (dims) for (size_t i = 0; i < h->net.dims.size(); ++i) dims[i] = h->net.dims[i];
+    if (out_legs) for (int q = 0; q < h->net.n_qubits; ++q) out_legs[q] = h->net.out_leg[q];
+  });
+}
+int tn_network_tensor(tn_network h, int32_t t, int32_t* rank, int32_t* inds, double* pos, double* data,
+                      int64_t data_cap) {
+  return guard([&] {
+    if (!h || t < 0 || t >= (int)h->net.tensors.size()) throw Err(TN_EINVAL, "bad tensor id");
+    const auto& T = h->net.tensors[t];
+    if (rank) *rank = (int32_t)T.inds.size();
+    if (inds) for (size_t k = 0; k < T.inds.size(); ++k) inds[k] = T.inds[k];
+    if (pos) { pos[0] = T.px; pos[1] = T.py; }
+    if (data) {
+      if (data_cap < (int64_t)T.data.size() * 2) throw Err(TN_EINVAL, "data buffer too small");
+      for (size_t k = 0; k < T.data.size(); ++k) { data[2 * k] = T.data[k].real(); data[2 * k + 1] = T.data[k].imag(); }
+    }
+  });
+}
+
+void tn_order_params_default(tn_order_params* p) {
+  if (!p) return;
+  tn::OrderParams d;
+  p->leaf_size = d.leaf_size; p->a_max = d.a_max; p->n_valid = d.n_valid; p->max_tries = d.max_tries;
+  p->n_seeds = d.n_seeds; p->max_log2_size = d.max_log2_size;
+}
+
+int tn_find_order(tn_network h, const tn_order_params* params, uint64_t seed, tn_order* out) {
+  return guard([&] {
+    if (!h || !out) throw Err(TN_EINVAL, "null");
+    tn::OrderParams p;
+    if (params) {
+      p.leaf_size = params->leaf_size; p.a_max = params->a_max; p.n_valid = params->n_valid;
+      p.max_tries = params->max_tries; p.n_seeds = params->n_seeds; p.max_log2_size = params->max_log2_size;
+    }
+    if (p.leaf_size < 1 || p.a_max < 1 || p.n_valid < 1 || p.max_tries < 1 || p.n_seeds < 1)
+      throw Err(TN_EINVAL, "tn_find_order: bad params");
+    auto o = std::make_unique<tn_order_s>();
+    o->ord = tn::find_order(h->net, seed, p);
+    o->net = &h->net;
+    *out = o.release();
+  });
+}
+void tn_order_free(tn_order o) { delete o; }
+
+int tn_order_get_info(tn_order o, tn_order_info* info) {
+  return guard([&] {
+    if (!o || !info) throw Err(TN_EINVAL, "null");
+    const auto& od = o->ord;
+    info->n_steps = (int32_t)od.steps.size();
+    info->n_slices = (int32_t)od.slices.size();
+    info->max_step_log2 = od.step_m.empty() ? 0 : *std::max_element(od.step_m.begin(), od.step_m.end());
+    info->max_size_log2 = od.step_res.empty() ? 0 : *std::max_element(od.step_res.begin(), od.step_res.end());
+    info->median_fallbacks = od.median_fallbacks;
+    info->log2_total_2M = od.total_2M > 0 ? std::log2(od.total_2M) : 0;
+    // one slice: drop the sliced bits of every step
+    auto kept = tn::kept_per_step(*o->net, od.steps);
+    std::set<int> sl(od.slices.begin(), od.slices.end());
+    int n = (int)o->net->tensors.size();
+    std::vector<std::vector<int>> node(n + od.steps.size());
+    for (int t = 0; t < n; ++t) node[t] = o->net->closed_inds(t);
+    double w = 0;
+    int64_t nsl = 1;
+    for (int i : od.slices) nsl *= o->net->dims[i];
+    for (size_t k = 0; k < od.steps.size(); ++k) {
+      std::set<int> u(node[od.steps[k].first].begin(), node[od.steps[k].first].end());
+      u.insert(node[od.steps[k].second].begin(), node[od.steps[k].second].end());
+      int m = 0;
+      for (int i : u) if (!sl.count(i)) m += o->net->log2dim(i);
+      w += std::ldexp(1.0, m + 1);
+      node[n + k] = kept[k];
+    }
+    info->log2_slice_2M = w > 0 ? std::log2(w) : 0;
+    info->n_slice_assignments = nsl;
+  });
+}
+int tn_order_steps(tn_order o, int32_t* steps) {
+  return guard([&] {
+    if (!o || !steps) throw Err(TN_EINVAL, "null");
+    for (size_t k = 0; k < o->ord.steps.size(); ++k) { steps[2 * k] = o->ord.steps[k].first; steps[2 * k + 1] = o->ord.steps[k].second; }
+  });
+}
+int tn_order_slices(tn_order o, int32_t* slices) {
+  return guard([&] {
+    if (!o) throw Err(TN_EINVAL, "null");
+    if (slices) for (size_t k = 0; k < o->ord.slices.size(); ++k) slices[k] = o->ord.slices[k];
+  });
+}
+
+int tn_plan_create(tn_network h, tn_order o, int32_t dtype, int32_t device, tn_plan* out) {
+  return guard([&] {
+    if (!h || !o || !out || o->net != &h->net) throw Err(TN_EINVAL, "tn_plan_create: bad handles");
+    if (dtype != TN_C64 && dtype != TN_C128) throw Err(TN_EINVAL, "bad dtype");
+    check_device(device);
+    auto p = std::make_unique<tn_plan_s>();
+    p->dtype = dtype;
+    p->device = device;
+    build_plan(*p, h->net, o->ord);
+    *out = p.release();
+  });
+}
+void tn_plan_free(tn_plan p) { delete p; }
+
+int tn_plan_get_info(tn_plan p, tn_plan_info* info) {
+  return guard([&] {
+    if (!p || !info) throw Err(TN_EINVAL, "null");
+    info->flops_per_slice = p->flops;
+    info->n_slices = p->n_slices;
+    info->arena_bytes = p->arena_bytes;
+    info->n_steps_small = p->n_small;
+    info->n_steps_tc = (int32_t)p->tcs.size();
+    info->n_launches_per_slice = (int32_t)p->kernels_per_slice;
+    info->tc_flops_per_slice = p->tc_flops;
+  });
+}
+
+int tn_plan_steps(tn_plan p, int32_t* out) {
+  return guard([&] {
+    if (!p || !out) throw Err(TN_EINVAL, "null");
+    std::copy(p->step_table.begin(), p->step_table.end(), out);
+  });
+}
+
+int tn_contract(tn_plan p, const uint8_t* bits, int64_t slice_begin, int64_t slice_end, double* amp, void* stream) {
+  return guard([&] {
+    if (!p || !amp || (!bits && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
+    cudaStream_t st = (cudaStream_t)stream;
+    run_slices(*p, bits, false, slice_begin, slice_end, st);
+    double h[2] = {0, 0};
+    if (p->dtype == TN_C64) {
+      float f[2];
+      CK(cudaMemcpyAsync(f, p->amp_d, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      h[0] = f[0]; h[1] = f[1];
+    } else {
+      CK(cudaMemcpyAsync(h, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    amp[0] = h[0];
+    amp[1] = h[1];
+  });
+}
+
+int tn_contract_device(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end, void* amp_dev,
+                       void* stream) {
+  return guard([&] {
+    if (!p || !amp_dev || (!bits_dev && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
+    cudaStream_t st = (cudaStream_t)stream;
+    run_slices(*p, bits_dev, true, slice_begin, slice_end, st);
+    if (p->dtype == TN_C64) add_amp_kernel<float><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    else add_amp_kernel<double><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    g_launches++;
+    CK(cudaGetLastError());
+  });
+}
+
+int tn_contract_profiled(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end, void* amp_dev,
+                         void* stream, tn_profile* prof) {
+  return guard([&] {
+    if (!p || !amp_dev || !prof || (!bits_dev && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
+    if (slice_begin < 0 || slice_end > p->n_slices || slice_begin > slice_end) throw Err(TN_EINVAL, "slice range");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(p->device));
+    if (p->net->n_qubits > 0) CK(cudaMemcpyAsync(p->bits_d, bits_dev, p->net->n_qubits, cudaMemcpyDeviceToDevice, st));
+    set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
+    CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
+    profile_slices(*p, slice_begin, slice_end, st, *prof);
+    if (p->dtype == TN_C64) add_amp_kernel<float><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    else add_amp_kernel<double><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    g_launches++;
+    CK(cudaGetLastError());
+  });
+}
+
+int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, void* stream) {
+  return guard([&] {
+    if (!p || !amps || n_bits < 0 || (!bits && n_bits > 0)) throw Err(TN_EINVAL, "null");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nq = p->net->n_qubits;
+    for (int j = 0; j < n_bits; ++j) {
+      run_slices(*p, bits + (size_t)j * nq, false, 0, p->n_slices, st);
+      if (p->dtype == TN_C64) {
+        float f[2];
+        CK(cudaMemcpyAsync(f, p->amp_d, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        amps[2 * j] = f[0]; amps[2 * j + 1] = f[1];
+      } else {
+        CK(cudaMemcpyAsync(amps + 2 * j, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+    }
+  });
+}
+
+int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t* inds_a, const void* B, int32_t rank_b,
+                     const int32_t* inds_b, void* C, int32_t rank_c, const int32_t* inds_c, const int32_t* dims,
+                     int32_t n_dims, int32_t path, void* stream) {
+  return guard([&] {
+    if (!A || !B || !C || !dims || rank_a < 0 || rank_b < 0 || rank_c < 0 || (rank_a && !inds_a) ||
+        (rank_b && !inds_b) || (rank_c && !inds_c))
+      throw Err(TN_EINVAL, "tn_contract_pair: null argument");
+    if (dtype != TN_C64 && dtype != TN_C128) throw Err(TN_EINVAL, "bad dtype");
+    std::vector<int> l2(n_dims);
+    for (int i = 0; i < n_dims; ++i) {
+      int d = dims[i], l = 0;
+      while ((1 << l) < d) ++l;
+      if (d < 1 || (1 << l) != d) throw Err(TN_EINVAL, "dimensions must be powers of two");
+      l2[i] = l;
+    }
+    auto chk = [&](const int32_t* ii, int r) {
+      std::vector<int> v(ii, ii + r);
+      for (int i : v) if (i < 0 || i >= n_dims) throw Err(TN_EINVAL, "index id out of range");
+      if (std::set<int>(v.begin(), v.end()).size() != v.size()) throw Err(TN_EINVAL, "repeated index");
+      return v;
+    };
+    NodeLayout LA, LB;
+    LA.inds = chk(inds_a, rank_a);
+    LB.inds = chk(inds_b, rank_b);
+    std::vector<int> ci = chk(inds_c, rank_c);
+    std::set<int> kept(ci.begin(), ci.end());
+    for (int i : ci)
+      if (!std::count(LA.inds.begin(), LA.inds.end(), i) && !std::count(LB.inds.begin(), LB.inds.end(), i))
+        throw Err(TN_EINVAL, "output index not in an operand");
+    Classes cl = classify(LA, LB, kept);
+    // C must be [batch][free of one operand][free of the other] (each group in C's order)
+    std::set<int> sbt(cl.batch.begin(), cl.batch.end()), sl(cl.lfree.begin(), cl.lfree.end()),
+        sr(cl.rfree.begin(), cl.rfree.end());
+    size_t nbt = cl.batch.size();
+    for (size_t k = 0; k < nbt; ++k)
+      if (!sbt.count(ci[k])) throw Err(TN_EUNSUPPORTED, "C must start with the batch indices");
+    bool l_first = nbt < ci.size() ? sl.count(ci[nbt]) > 0 : true;
+    std::vector<int> g1(ci.begin() + nbt, ci.begin() + nbt + (l_first ? cl.lfree.size() : cl.rfree.size()));
+    std::vector<int> g2(ci.begin() + nbt + g1.size(), ci.end());
+    for (int i : g1) if (!(l_first ? sl : sr).count(i)) throw Err(TN_EUNSUPPORTED, "C groups must be contiguous");
+    for (int i : g2) if (!(l_first ? sr : sl).count(i)) throw Err(TN_EUNSUPPORTED, "C groups must be contiguous");
+    std::vector<int> batch(ci.begin(), ci.begin() + nbt);
+    int nb = sum_bits(batch, l2), kk = sum_bits(cl.contr, l2);
+    const NodeLayout& LX = l_first ? LA : LB;
+    const NodeLayout& LY = l_first ? LB : LA;
+    int mx = sum_bits(g1, l2), my = sum_bits(g2, l2);
+    bool tc = path == TN_PATH_TC || (path == TN_PATH_AUTO && want_tc(dtype, nb, mx, my, kk));
+    if (tc && (dtype != TN_C64 || kk < 4)) throw Err(TN_EUNSUPPORTED, "tensor-core path needs complex64 and K >= 16");
+    cudaStream_t st = (cudaStream_t)stream;
+    int cur = 0;
+    CK(cudaGetDevice(&cur));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cur));
+    if (prop.major != 10) throw Err(TN_ECUDA, "sm_100 device required");
+    TabPool pool;
+    std::vector<void*> ptrs = {const_cast<void*>(l_first ? A : B), const_cast<void*>(l_first ? B : A), C};
+    std::vector<void*> allocs;
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      CK(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
+      allocs.push_back(p);
+      return p;
+    };
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    void** ptrs_d = (void**)dalloc(3 * sizeof(void*));
+    h2d(ptrs_d, ptrs.data(), 3 * sizeof(void*));
+    if (tc) {
+      TcStep t;
+      t.nb_bits = nb; t.m_bits = mx; t.n_bits = my; t.k_bits = kk;
+      t.BN = my >= 7 ? 128 : 64;
+      t.c_node = 2;
+      t.px.src = 0; t.px.nb_bits = nb; t.px.r_bits = mx; t.px.k_bits = kk;
+      t.px.gb = pool.add(group_of(batch, LX, l2)); t.px.gr = pool.add(group_of(g1, LX, l2));
+      t.px.gk = pool.add(group_of(cl.contr, LX, l2));
+      t.py.src = 1; t.py.nb_bits = nb; t.py.r_bits = my; t.py.k_bits = kk;
+      t.py.gb = pool.add(group_of(batch, LY, l2)); t.py.gr = pool.add(group_of(g2, LY, l2));
+      t.py.gk = pool.add(group_of(cl.contr, LY, l2));
+      size_t xb = size_t(12) << (nb + mx + kk), yb = size_t(12) << (nb + my + kk);
+      char* scratch = (char*)dalloc(xb + yb + 2 * ALIGN);
+      int64_t* tab_d = (int64_t*)dalloc(pool.v.size() * 8);
+      h2d(tab_d, pool.v.data(), pool.v.size() * 8);
+      t.x_off = 0;
+      t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
+      t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128);
+      t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN);
+      launch_tc(t, scratch, ptrs_d, tab_d, st);
+      CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies
+    } else {
+      SmallStep d{};
+      d.a = 0; d.b = 1; d.c = 2;
+      d.nb_bits = nb; d.m_bits = mx; d.n_bits = my; d.k_bits = kk;
+      d.Ab = pool.add(group_of(batch, LX, l2)); d.Am = pool.add(group_of(g1, LX, l2));
+      d.Ak = pool.add(group_of(cl.contr, LX, l2));
+      d.Bb = pool.add(group_of(batch, LY, l2)); d.Bk = pool.add(group_of(cl.contr, LY, l2));
+      d.Bn = pool.add(group_of(g2, LY, l2));
+      Wave w;
+      w.steps = {d};
+      int64_t outs = int64_t(1) << (nb + mx + my);
+      w.prefix = {0, (outs + OUTS_PER_CTA - 1) / OUTS_PER_CTA};
+      w.n_cta = w.prefix[1];
+      w.steps_d = (SmallStep*)dalloc(sizeof(SmallStep));
+      h2d(w.steps_d, w.steps.data(), sizeof(SmallStep));
+      w.prefix_d = (int64_t*)dalloc(2 * sizeof(int64_t));
+      h2d(w.prefix_d, w.prefix.data(), 2 * sizeof(int64_t));
+      int64_t* tab_d = (int64_t*)dalloc(pool.v.size() * 8);
+      h2d(tab_d, pool.v.data(), pool.v.size() * 8);
+      if (dtype == TN_C64) launch_wave<float>(w, ptrs_d, tab_d, st);
+      else launch_wave<double>(w, ptrs_d, tab_d, st);
+      CK(cudaStreamSynchronize(st));
+    }
+    for (void* p : allocs) CK(cudaFreeAsync(p, st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI against the oracle.
+
+Tolerances:
+  * step level, complex128 (CUDA-core DFMA): |C - C_ref| <= 1e-12 * sum_k |A||B|
+  * step level, complex64 (bf16x6 tensor cores / fp32 FMA): |C - C_ref| <= 2e-6 * sum_k |A||B|
+    (fp32 storage of A, B contributes 2^-24 relative per product; bf16x6 drops terms
+    below 2^-24; fp32 accumulation adds <= K * 2^-24 in the worst case, ~sqrt(K) typically)
+  * amplitudes: complex128 |a - a_ref| <= 1e-10 * max(|a_ref|, 2^{-n/2});
+    complex64 |a - a_ref| <= 1e-5 * max(|a_ref|, 2^{-n/2})  (BASELINE north_star, with the
+    RMS amplitude 2^{-n/2} as the scale for amplitudes near zero)
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from tn_inputs import config_circuit, lattice_cz, iqp, sycamore, random_bitstrings, concat, inverse_circuit
+from oracle.network import build_network
+from oracle.ssa import find_order, choose_slices
+from oracle.contract import contract_tree, contract_pair as oracle_pair
+
+import paper_2208_01498_b200 as tb
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _rand(shape, seed, dtype):
+    g = np.random.default_rng(seed)
+    x = (g.standard_normal(shape) + 1j * g.standard_normal(shape)) / math.sqrt(2)
+    return x.astype(np.complex64 if dtype == tb.TN_C64 else np.complex128)
+
+
+def _run_pair(inds_a, inds_b, inds_c, dims, dtype, path, seed=0):
+    dev = _cuda()
+    sa = [dims[i] for i in inds_a]
+    sb = [dims[i] for i in inds_b]
+    sc = [dims[i] for i in inds_c]
+    A = _rand(sa, seed, dtype)
+    B = _rand(sb, seed + 1, dtype)
+    tdt = torch.complex64 if dtype == tb.TN_C64 else torch.complex128
+    tA = torch.from_numpy(A).to(dev)
+    tB = torch.from_numpy(B).to(dev)
+    tC = torch.full(sc, float("nan"), dtype=tdt, device=dev)
+    torch.cuda.synchronize()
+    tb.contract_pair(dtype, tA.data_ptr(), inds_a, tB.data_ptr(), inds_b, tC.data_ptr(), inds_c, dims, path)
+    torch.cuda.synchronize()
+    got = tC.cpu().numpy()
+    ref_inds, ref = oracle_pair(list(inds_a), A.astype(np.complex128), list(inds_b), B.astype(np.complex128),
+                                inds_c, dims)
+    _, bound = oracle_pair(list(inds_a), np.abs(A).astype(np.complex128), list(inds_b),
+                           np.abs(B).astype(np.complex128), inds_c, dims)
+    perm = [ref_inds.index(i) for i in inds_c]
+    ref = np.transpose(ref, perm) if perm else ref
+    bound = np.abs(np.transpose(bound, perm) if perm else bound)
+    return got, ref, bound
+
+
+PAIR_CASES = [
+    # (inds_a, inds_b, inds_c, dims) -- index ids are positions in dims
+    ([0, 1], [1, 2], [0, 2], [2, 2, 2]),                                  # 2x2 matrix product
+    ([0, 1, 2], [2, 3, 1], [0, 3], [2, 4, 2, 2]),                          # two contracted, dim 4
+    ([0, 1, 2], [0, 2, 3], [0, 1, 3], [2, 2, 2, 2]),                       # batch (hyperedge) index
+    ([3, 0, 1, 2], [4, 2, 1], [0, 3, 4], [2, 2, 2, 2, 2]),                 # permuted operand layouts
+    ([0], [1], [0, 1], [2, 2]),                                            # outer product
+    ([0, 1], [0, 1], [], [2, 4]),                                          # full contraction to a scalar
+]
+
+
+@pytest.mark.parametrize("dtype", [tb.TN_C64, tb.TN_C128])
+@pytest.mark.parametrize("case", range(len(PAIR_CASES)))
+def test_pair_small_path(case, dtype):
+    ia, ib, ic, dims = PAIR_CASES[case]
+    got, ref, bound = _run_pair(ia, ib, ic, dims, dtype, tb.TN_PATH_SMALL, seed=case)
+    tol = 2e-6 if dtype == tb.TN_C64 else 1e-12
+    assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
+
+
+def _gemm_case(nb, m, n, k, perm_seed=None):
+    """indices: batch b0.., rows m.., cols n.., contracted k.. each of dim 2."""
+    ids = list(range(nb + m + n + k))
+    bt, mm, nn, kk = ids[:nb], ids[nb:nb + m], ids[nb + m:nb + m + n], ids[nb + m + n:]
+    ia = bt + mm + kk
+    ib = bt + kk + nn
+    if perm_seed is not None:
+        g = np.random.default_rng(perm_seed)
+        ia = list(g.permutation(ia))
+        ib = list(g.permutation(ib))
+    return ia, ib, bt + mm + nn, [2] * len(ids)
+
+
+TC_CASES = [
+    (0, 7, 7, 4, None),       # exactly one 128x128 tile, K = 16
+    (0, 6, 5, 4, None),       # ragged: M = 64 < 128, N = 32 < BN
+    (0, 9, 8, 9, None),       # 4 x 2 tiles, K = 512 (16 stages)
+    (2, 7, 6, 5, 3),          # batch 4, permuted layouts folded into the pack
+    (0, 10, 10, 12, 5),       # several tiles, K = 4096, permuted
+]
+
+
+@pytest.mark.parametrize("case", range(len(TC_CASES)))
+def test_pair_tensor_core_path(case):
+    nb, m, n, k, ps = TC_CASES[case]
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=10 + case)
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-6 * bound + 1e-30), (err / bound).max()
+
+
+def test_pair_tc_matches_small_path():
+    ia, ib, ic, dims = _gemm_case(1, 7, 7, 6, 9)
+    g1, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=3)
+    g2, _, _ = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_SMALL, seed=3)
+    assert np.all(np.abs(g1 - g2) <= 4e-6 * bound + 1e-30)
+
+
+# ------------------------------------------------------------------ plans ----
+def _amp_tol(dtype, n):
+    return (1e-10 if dtype == tb.TN_C128 else 1e-5), 2.0 ** (-n / 2)
+
+
+def _plan_vs_oracle(circ, dtype, seed, hyper=False, max_log2_size=0, n_bits=4, with_zero=True):
+    _cuda()
+    on = build_network(circ, diag_hyper=hyper)
+    osteps, _ = find_order(on, seed=seed)
+    cn = tb.Network.from_circuit(circ, diag_hyper=hyper)
+    co = tb.Order(cn, seed=seed, max_log2_size=max_log2_size)
+    assert co.steps() == osteps                       # bit-identical order
+    plan = tb.Plan(cn, co, dtype=dtype)
+    bits = random_bitstrings(circ.n, n_bits, seed)
+    if with_zero:
+        bits = np.vstack([np.zeros((1, circ.n), np.uint8), bits])
+    got = plan.amplitudes(bits)
+    tol, scale = _amp_tol(dtype, circ.n)
+    for x, g in zip(bits, got):
+        want = contract_tree(on, osteps, x)
+        assert abs(g - want) <= tol * max(abs(want), scale), (x, g, want)
+    return plan
+
+
+def test_config0_complex128_all_bitstrings():
+    """configs[0]: 4x4 depth 8, complex128, <0|C|0> + 16 seeded bitstrings."""
+    _plan_vs_oracle(config_circuit(0), tb.TN_C128, seed=0, n_bits=16)
+
+
+def test_config0_complex64():
+    _plan_vs_oracle(config_circuit(0), tb.TN_C64, seed=0, n_bits=16)
+
+
+def test_plan_with_slicing_matches_unsliced_oracle():
+    c = lattice_cz(5, 5, 8, 4)
+    plan = _plan_vs_oracle(c, tb.TN_C128, seed=1, max_log2_size=12, n_bits=3)
+    assert plan.info()["n_slices"] > 1
+
+
+def test_plan_slices_partition_the_amplitude():
+    c = lattice_cz(4, 5, 8, 6)
+    cn = tb.Network.from_circuit(c)
+    co = tb.Order(cn, seed=2, max_log2_size=10)
+    plan = tb.Plan(cn, co, dtype=tb.TN_C128)
+    ns = plan.info()["n_slices"]
+    x = random_bitstrings(c.n, 1, 5)[0]
+    full = plan.contract(x)
+    parts = sum(plan.contract(x, s, s + 1) for s in range(ns))
+    assert abs(full - parts) < 1e-12
+
+
+def test_iqp_hyperedges_complex128():
+    _plan_vs_oracle(iqp(5, 2, 7), tb.TN_C128, seed=3, hyper=True, n_bits=6)
+
+
+def test_sycamore_small_complex64():
+    _plan_vs_oracle(sycamore(4, 3), tb.TN_C64, seed=4, n_bits=2, max_log2_size=22)
+
+
+def test_plan_uses_tensor_cores_and_matches_oracle():
+    """6x6 depth 12: several GEMM-shaped steps go to tcgen05 inside one plan."""
+    c = lattice_cz(6, 6, 12, 8)
+    plan = _plan_vs_oracle(c, tb.TN_C64, seed=5, n_bits=2, with_zero=False)
+    assert plan.info()["n_steps_tc"] >= 1
+
+
+def test_c_then_cdagger_identity_on_gpu():
+    c = lattice_cz(5, 5, 6, 9)
+    cc = concat(c, inverse_circuit(c))
+    cn = tb.Network.from_circuit(cc)
+    co = tb.Order(cn, seed=0, max_log2_size=24)
+    plan = tb.Plan(cn, co, dtype=tb.TN_C64)
+    assert abs(plan.contract(np.zeros(c.n, np.uint8)) - 1.0) < 1e-5
+
+
+def test_contract_device_accumulates_on_device():
+    dev = _cuda()
+    c = config_circuit(0)
+    cn = tb.Network.from_circuit(c)
+    co = tb.Order(cn, seed=0)
+    plan = tb.Plan(cn, co, dtype=tb.TN_C128)
+    x = random_bitstrings(c.n, 1, 1)[0]
+    bits = torch.from_numpy(x).to(dev)
+    amp = torch.zeros(1, dtype=torch.complex128, device=dev)
+    plan.contract_device(bits.data_ptr(), 0, 1, amp.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    plan.contract_device(bits.data_ptr(), 0, 1, amp.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert abs(amp.item() - 2 * plan.contract(x)) < 1e-13
+
+
+# ------------------------------------------------ full-size config 1 ------
+def test_config1_full_size_biggest_gemm_sampled():
+    """configs[1] (8x8 depth 16, complex64): build the bench plan, take its largest
+    tensor-core step shape and run that GEMM (same kernel, tile and grid) on random
+    operands; check 64 sampled outputs against complex128 dot products."""
+    dev = _cuda()
+    c = config_circuit(1)
+    cn = tb.Network.from_circuit(c)
+    co = tb.Order(cn, seed=0, max_log2_size=31)
+    plan = tb.Plan(cn, co, dtype=tb.TN_C64)
+    st = plan.steps()
+    tc = st[st[:, 0] == tb.TN_PATH_TC]
+    assert len(tc) > 0
+    big = tc[np.argmax(tc[:, 1] + tc[:, 2] + tc[:, 3] + tc[:, 4])]
+    nb, m, n, k = (int(v) for v in big[1:5])
+    del plan
+    torch.cuda.empty_cache()
+    B_, M_, N_, K_ = 1 << nb, 1 << m, 1 << n, 1 << k
+    g = torch.Generator(device=dev).manual_seed(1)
+    A = torch.randn(B_, M_, K_, dtype=torch.complex64, device=dev, generator=g)
+    Bm = torch.randn(B_, K_, N_, dtype=torch.complex64, device=dev, generator=g)
+    Cm = torch.empty(B_, M_, N_, dtype=torch.complex64, device=dev)
+    ids = list(range(nb + m + n + k))
+    bt, mm, nn, kk = ids[:nb], ids[nb:nb + m], ids[nb + m:nb + m + n], ids[nb + m + n:]
+    tb.contract_pair(tb.TN_C64, A.data_ptr(), bt + mm + kk, Bm.data_ptr(), bt + kk + nn, Cm.data_ptr(),
+                     bt + mm + nn, [2] * len(ids), tb.TN_PATH_TC)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    for _ in range(64):
+        b, i, j = int(rng.integers(B_)), int(rng.integers(M_)), int(rng.integers(N_))
+        a_row = A[b, i, :].cpu().numpy().astype(np.complex128)
+        b_col = Bm[b, :, j].cpu().numpy().astype(np.complex128)
+        want = np.dot(a_row, b_col)
+        bound = np.dot(np.abs(a_row), np.abs(b_col))
+        assert abs(Cm[b, i, j].item() - want) <= 2e-6 * bound

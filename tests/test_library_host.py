@@ -1,0 +1,93 @@
+"""C-ABI library, host side (CPU, -m "not gpu"): symbols, network construction and
+the order/slicing search compared with the oracle -- bit-identical orders."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tn_inputs import config_circuit, lattice_cz, iqp, sycamore, random3d
+from oracle.network import build_network
+from oracle.ssa import find_order, choose_slices
+
+import paper_2208_01498_b200 as tb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tn.h")).read()
+    declared = set(re.findall(r"\b(tn_[a-z0-9_]+)\s*\(", hdr))
+    declared -= {"tn_network_s", "tn_order_s", "tn_plan_s"}
+    lib = ctypes.CDLL(tb._lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert declared == set(tb.EXPORTED_SYMBOLS)
+
+
+def test_errors_are_reported_not_fatal():
+    with pytest.raises(tb.TnError, match="bad qubit"):
+        tb.Network(2, np.zeros((2, 2)), np.array([[0, 5]], np.int32), np.zeros(16, np.complex128))
+    with pytest.raises(tb.TnError):
+        tb.Network(0, np.zeros((0, 2)), np.zeros((0, 2), np.int32), np.zeros(0, np.complex128))
+
+
+def _compare_networks(c, hyper):
+    on = build_network(c, diag_hyper=hyper)
+    cn = tb.Network.from_circuit(c, diag_hyper=hyper)
+    inf = cn.info()
+    d, o = cn.dims()
+    assert inf["n_tensors"] == len(on.tensors)
+    assert list(d) == on.dims and list(o) == on.out_leg
+    assert inf["radius"] == on.radius and inf["k_bound"] == on.k_bound
+    for t, T in enumerate(on.tensors):
+        inds, pos, data = cn.tensor(t)
+        assert list(inds) == T.inds and tuple(pos) == T.pos
+        assert np.max(np.abs(data - T.data)) <= 1e-13
+    return on, cn
+
+
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4])
+def test_network_identical_to_oracle(ci):
+    _compare_networks(config_circuit(ci), hyper=(ci == 3))
+
+
+@pytest.mark.parametrize("case", ["c0", "c3", "small_slice", "syc_small", "r3d_small"])
+def test_order_and_slices_bit_identical(case):
+    if case == "c0":
+        c, hyper, seed, tgt = config_circuit(0), False, 11, 0
+    elif case == "c3":
+        c, hyper, seed, tgt = iqp(6, 2, 3), True, 5, 14
+    elif case == "small_slice":
+        c, hyper, seed, tgt = lattice_cz(5, 5, 8, 2), False, 3, 14
+    elif case == "syc_small":
+        c, hyper, seed, tgt = sycamore(4, 1), False, 2, 20
+    else:
+        c, hyper, seed, tgt = random3d(6, 6, 1, n_patches=1), False, 9, 16
+    on, cn = _compare_networks(c, hyper)
+    co = tb.Order(cn, seed=seed, max_log2_size=tgt)
+    os_, _ = find_order(on, seed=seed)
+    assert co.steps() == os_
+    if tgt:
+        assert co.slices() == choose_slices(on, os_, tgt)
+
+
+@pytest.mark.slow
+def test_order_bit_identical_config1():
+    c = config_circuit(1)
+    on, cn = _compare_networks(c, False)
+    co = tb.Order(cn, seed=7, max_log2_size=30)
+    os_, _ = find_order(on, seed=7)
+    assert co.steps() == os_
+    assert co.slices() == choose_slices(on, os_, 30)
+
+
+def test_order_info_consistent():
+    c = lattice_cz(4, 4, 8, 0)
+    cn = tb.Network.from_circuit(c)
+    o = tb.Order(cn, seed=1, max_log2_size=6)
+    inf = o.info()
+    assert inf["n_steps"] == cn.info()["n_tensors"] - 1
+    assert inf["n_slice_assignments"] == 2 ** inf["n_slices"]
+    assert inf["log2_slice_2M"] <= inf["log2_total_2M"] + 1e-9
