@@ -24,6 +24,8 @@ __device__ __forceinline__ int64_t gmap(const int64_t* __restrict__ tab, const G
 struct SmallStep {
   int32_t a, b, c;                 // node ids in the device pointer table
   int32_t nb_bits, m_bits, n_bits, k_bits;
+  int32_t g_log2;                  // log2 threads cooperating on one output (0, 5 or 7)
+  int32_t opc;                     // outputs per CTA
   int32_t pad;
   GroupMap Ab, Am, Ak, Bb, Bk, Bn;
 };

@@ -13,8 +13,9 @@
 //
 // Pipeline: pack kernel (fused permutation to matricised [b][rows][k] form + bf16x3
 // split, one HBM pass) -> TMA (SWIZZLE_64B, 3-D maps over planes) into a 2/3-stage
-// mbarrier ring -> one elected thread issues tcgen05.mma -> tcgen05.ld epilogue
-// writes interleaved complex64 C.
+// mbarrier ring -> one elected thread issues tcgen05.mma into ping-pong TMEM buffers
+// -> epilogue warps promote each stage into fp32 registers (tcgen05.ld) and finally
+// write interleaved complex64 C (or a split-K partial).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -77,7 +78,10 @@ struct Cfg {
   static constexpr int B_PLANE = BN * BK * 2;
   static constexpr int STAGE = 6 * A_PLANE + 6 * B_PLANE;
   static constexpr int STAGES = (3 * STAGE + 2048 <= 227 * 1024) ? 3 : 2;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int ACC_COLS = 2 * BN;                  // re + im of one accumulator buffer
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;           // ping-pong buffers
+  static constexpr int EPI_WARPS = 4 * (BN / 64);          // each owns 32 rows x 64 columns
+  static constexpr int THREADS = 32 * (EPI_WARPS + 2);     // + TMA warp + MMA warp
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -89,6 +93,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -129,32 +136,49 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 
+// Precision: the tensor core's fp32 accumulation
+// truncates, so an accumulator updated T times drifts by ~T/4 ulp toward zero.  Each
+// 32-wide K stage is therefore accumulated in a fresh TMEM buffer (24 MMA updates per
+// element) and promoted by the epilogue warps into fp32 registers with round-to-
+// nearest adds; two TMEM buffers ping-pong so promotion overlaps the next stage.
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_bf16x6_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
-                        int32_t nb, int32_t transpose_c) {
+                        int32_t nb, int32_t kc_per_split, float2* __restrict__ partial) {
   using CF = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE);
   uint64_t* empty = full + CF::STAGES;
-  uint64_t* accum = empty + CF::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + CF::STAGES;     // [2] MMA -> epilogue: buffer holds a finished stage
+  uint64_t* tempty = tfull + 2;             // [2] epilogue -> MMA: buffer promoted
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_blk = blockIdx.x, m_blk = blockIdx.y, b = blockIdx.z;
-  const int nk = (K + BK - 1) / BK;
+  const int TMA_WARP = CF::EPI_WARPS, MMA_WARP = CF::EPI_WARPS + 1;
+  // split-K: blockIdx.z = split * nb + batch; this CTA covers K chunks [kc0, kc0 + nk)
+  const int n_blk = blockIdx.x, m_blk = blockIdx.y, b = blockIdx.z % nb, split = blockIdx.z / nb;
+  const int nk_all = (K + BK - 1) / BK;
+  const int kc0 = split * kc_per_split;
+  const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(accum, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CF::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
-  if (warp == 2) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(CF::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -164,104 +188,121 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % CF::STAGES;
-      const uint32_t ph = (kc / CF::STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], CF::STAGE);
-      uint8_t* st = smem + s * CF::STAGE;
-      for (int p = 0; p < 6; ++p)
-        tma_load_3d(&tmA, st + p * CF::A_PLANE, &full[s], kc * BK, m_blk * BM, p * nb + b);
-      for (int p = 0; p < 6; ++p)
-        tma_load_3d(&tmB, st + 6 * CF::A_PLANE + p * CF::B_PLANE, &full[s], kc * BK, n_blk * BN, p * nb + b);
+  if (warp == TMA_WARP) {
+    if (lane == 0) {
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % CF::STAGES;
+        const uint32_t ph = (kc / CF::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], CF::STAGE);
+        uint8_t* st = smem + s * CF::STAGE;
+        for (int p = 0; p < 6; ++p)
+          tma_load_3d(&tmA, st + p * CF::A_PLANE, &full[s], (kc0 + kc) * BK, m_blk * BM, p * nb + b);
+        for (int p = 0; p < 6; ++p)
+          tma_load_3d(&tmB, st + 6 * CF::A_PLANE + p * CF::B_PLANE, &full[s], (kc0 + kc) * BK, n_blk * BN, p * nb + b);
+      }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer (single thread) ----
-    // idesc: F32 accumulate, BF16 A/B, K-major both, N = BN, M = 128
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    const uint32_t idesc_negA = idesc | (1u << 13);
-    const uint32_t t_re = tmem, t_im = tmem + BN;
-    // (piece of A, piece of B) with i + j <= 2
-    const int PA[6] = {0, 0, 1, 0, 1, 2};
-    const int PB[6] = {0, 1, 0, 2, 1, 0};
+  } else if (warp == MMA_WARP) {
+    if (lane == 0) {
+      // idesc: F32 accumulate, BF16 A/B, K-major both, N = BN, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      const uint32_t idesc_negA = idesc | (1u << 13);
+      const int PA[6] = {0, 0, 1, 0, 1, 2};
+      const int PB[6] = {0, 1, 0, 2, 1, 0};
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % CF::STAGES;
+        const uint32_t ph = (kc / CF::STAGES) & 1;
+        const int buf = kc & 1;
+        const uint32_t tph = (kc >> 1) & 1;
+        mbar_wait(&tempty[buf], tph ^ 1);       // epilogue has drained this buffer
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
+        uint8_t* st = smem + s * CF::STAGE;
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks) {
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t b_re = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t b_im = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint32_t acc = (ks | q) != 0;   // fresh accumulator every stage
+            mma_bf16(t_re, a_re, b_re, idesc, acc);
+            mma_bf16(t_re, a_im, b_im, idesc_negA, 1);
+            mma_bf16(t_im, a_re, b_im, idesc, acc);
+            mma_bf16(t_im, a_im, b_re, idesc, 1);
+          }
+        }
+        mma_commit(&empty[s]);     // smem stage free once these MMAs have read it
+        mma_commit(&tfull[buf]);   // accumulator buffer ready for promotion
+      }
+    }
+  } else {
+    // ---- epilogue warps: promote every stage into fp32 registers ----
+    const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
+    const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
+    const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+    float ar[64], ai[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
     for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % CF::STAGES;
-      const uint32_t ph = (kc / CF::STAGES) & 1;
-      mbar_wait(&full[s], ph);
+      const int buf = kc & 1;
+      const uint32_t tph = (kc >> 1) & 1;
+      mbar_wait(&tfull[buf], tph);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint8_t* st = smem + s * CF::STAGE;
+      const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;
 #pragma unroll
-      for (int ks = 0; ks < BK / 16; ++ks) {
+      for (int c = 0; c < 64; c += 16) {
+        uint32_t vr[16], vi[16];
+        tmem_ld16(t_re + c, vr);
+        tmem_ld16(t_im + c, vi);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
-          const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
-          const uint64_t b_re = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
-          const uint64_t b_im = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
-          const uint32_t acc = (kc | ks | q) != 0;
-          mma_bf16(t_re, a_re, b_re, idesc, acc);
-          mma_bf16(t_re, a_im, b_im, idesc_negA, 1);
-          mma_bf16(t_im, a_re, b_im, idesc, acc);
-          mma_bf16(t_im, a_im, b_re, idesc, 1);
+        for (int j = 0; j < 16; ++j) {
+          ar[c + j] = __fadd_rn(ar[c + j], __uint_as_float(vr[j]));
+          ai[c + j] = __fadd_rn(ai[c + j], __uint_as_float(vi[j]));
         }
       }
-      mma_commit(&empty[s]);   // frees the stage once these MMAs have read it
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
-    mma_commit(accum);
-  }
-  __syncwarp();
-
-  // ---- epilogue: TMEM -> registers -> interleaved complex64 ----
-  mbar_wait(accum, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  float2* C = reinterpret_cast<float2*>(ptrs[c_node]);
-  const int row = m_blk * BM + warp * 32 + lane;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    uint32_t re[32], im[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(re[0]), "=r"(re[1]), "=r"(re[2]), "=r"(re[3]), "=r"(re[4]), "=r"(re[5]), "=r"(re[6]), "=r"(re[7]),
-          "=r"(re[8]), "=r"(re[9]), "=r"(re[10]), "=r"(re[11]), "=r"(re[12]), "=r"(re[13]), "=r"(re[14]), "=r"(re[15]),
-          "=r"(re[16]), "=r"(re[17]), "=r"(re[18]), "=r"(re[19]), "=r"(re[20]), "=r"(re[21]), "=r"(re[22]), "=r"(re[23]),
-          "=r"(re[24]), "=r"(re[25]), "=r"(re[26]), "=r"(re[27]), "=r"(re[28]), "=r"(re[29]), "=r"(re[30]), "=r"(re[31])
-        : "r"(tmem + lane_base + c0));
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(im[0]), "=r"(im[1]), "=r"(im[2]), "=r"(im[3]), "=r"(im[4]), "=r"(im[5]), "=r"(im[6]), "=r"(im[7]),
-          "=r"(im[8]), "=r"(im[9]), "=r"(im[10]), "=r"(im[11]), "=r"(im[12]), "=r"(im[13]), "=r"(im[14]), "=r"(im[15]),
-          "=r"(im[16]), "=r"(im[17]), "=r"(im[18]), "=r"(im[19]), "=r"(im[20]), "=r"(im[21]), "=r"(im[22]), "=r"(im[23]),
-          "=r"(im[24]), "=r"(im[25]), "=r"(im[26]), "=r"(im[27]), "=r"(im[28]), "=r"(im[29]), "=r"(im[30]), "=r"(im[31])
-        : "r"(tmem + lane_base + BN + c0));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-      if (!transpose_c) {
-        float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + n_blk * BN + c0;
-        const int lim = N - (n_blk * BN + c0);
-        if (lim >= 32) {
+    // single split: write C; several: this split's fp32 partial (reduced in fp64 later)
+    float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
+    const int row = m_blk * BM + lg * 32 + lane;
+    const int col0 = n_blk * BN + ch * 64;
+    if (row < M && col0 < N) {
+      float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
+      if (N - col0 >= 64) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            *reinterpret_cast<float4*>(crow + j) =
-                make_float4(__uint_as_float(re[j]), __uint_as_float(im[j]), __uint_as_float(re[j + 1]), __uint_as_float(im[j + 1]));
-        } else {
-          for (int j = 0; j < 32 && j < lim; ++j) crow[j] = make_float2(__uint_as_float(re[j]), __uint_as_float(im[j]));
-        }
+        for (int j = 0; j < 64; j += 2) *reinterpret_cast<float4*>(crow + j) = make_float4(ar[j], ai[j], ar[j + 1], ai[j + 1]);
       } else {
-        // C stored [b][n][m]: consecutive lanes write consecutive m (coalesced)
-        for (int j = 0; j < 32; ++j) {
-          const int col = n_blk * BN + c0 + j;
-          if (col < N) C[((int64_t)b * N + col) * (int64_t)M + row] = make_float2(__uint_as_float(re[j]), __uint_as_float(im[j]));
-        }
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < N - col0) crow[j] = make_float2(ar[j], ai[j]);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+  if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
 }
 
 }  // namespace tc
+
+// C[i] = sum_s partial[s][i], summed in fp64 (split-K epilogue)
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float2* __restrict__ partial, int32_t S,
+                                                            int64_t n, void* const* __restrict__ ptrs, int32_t c_node) {
+  float2* C = reinterpret_cast<float2*>(ptrs[c_node]);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < S; ++s) {
+      const float2 v = partial[(int64_t)s * n + i];
+      re += v.x;
+      im += v.y;
+    }
+    C[i] = make_float2((float)re, (float)im);
+  }
+}
 }  // namespace tnd

@@ -8,11 +8,17 @@
 
 namespace tnd {
 
+// Accumulation is in fp64 for both complex64 and complex128 (the small path is
+// latency/HBM bound, so the wider FMA is free; it removes the K-length fp32
+// random-walk error of long reductions).  Long reductions with few outputs split K
+// over a warp (g_log2 = 5) or the whole CTA (g_log2 = 7), reduced by shuffles and
+// shared memory in fp64.
 template <typename R>
 __global__ void __launch_bounds__(128) small_contract_kernel(
     const SmallStep* __restrict__ steps, const int64_t* __restrict__ cta_prefix, int32_t n_steps,
-    const int64_t* __restrict__ tab, void* const* __restrict__ ptrs, int32_t outs_per_cta) {
+    const int64_t* __restrict__ tab, void* const* __restrict__ ptrs, int32_t /*unused*/) {
   using C2 = typename cplx_t<R>::type;
+  __shared__ double red[2][4];
   // step of this CTA: last s with cta_prefix[s] <= blockIdx.x
   int lo = 0, hi = n_steps - 1;
   while (lo < hi) {
@@ -23,27 +29,47 @@ __global__ void __launch_bounds__(128) small_contract_kernel(
   const C2* __restrict__ A = reinterpret_cast<const C2*>(ptrs[d.a]);
   const C2* __restrict__ B = reinterpret_cast<const C2*>(ptrs[d.b]);
   C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[d.c]);
-  const int64_t start = ((int64_t)blockIdx.x - cta_prefix[lo]) * outs_per_cta;
+  const int64_t start = ((int64_t)blockIdx.x - cta_prefix[lo]) * d.opc;
   const int64_t total = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
-  const int64_t end = min(total, start + outs_per_cta);
+  const int64_t end = min(total, start + d.opc);
   const int64_t K = int64_t(1) << d.k_bits;
   const int64_t nmask = (int64_t(1) << d.n_bits) - 1, mmask = (int64_t(1) << d.m_bits) - 1;
-  for (int64_t o = start + threadIdx.x; o < end; o += blockDim.x) {
-    const int64_t n = o & nmask;
-    const int64_t m = (o >> d.n_bits) & mmask;
-    const int64_t bb = o >> (d.n_bits + d.m_bits);
-    const int64_t ao = gmap(tab, d.Ab, bb) + gmap(tab, d.Am, m);
-    const int64_t bo = gmap(tab, d.Bb, bb) + gmap(tab, d.Bn, n);
-    R re = 0, im = 0;
-    for (int64_t k = 0; k < K; ++k) {
-      const C2 a = A[ao + gmap(tab, d.Ak, k)];
-      const C2 b = B[bo + gmap(tab, d.Bk, k)];
-      re = fma(a.x, b.x, re);
-      re = fma(-a.y, b.y, re);
-      im = fma(a.x, b.y, im);
-      im = fma(a.y, b.x, im);
+  const int G = 1 << d.g_log2;
+  const int gl = threadIdx.x & (G - 1);
+  const int per = blockDim.x >> d.g_log2;       // outputs in flight per CTA
+  for (int64_t o0 = start; o0 < end; o0 += per) {
+    const int64_t o = o0 + (threadIdx.x >> d.g_log2);
+    double re = 0.0, im = 0.0;
+    if (o < end) {
+      const int64_t n = o & nmask;
+      const int64_t m = (o >> d.n_bits) & mmask;
+      const int64_t bb = o >> (d.n_bits + d.m_bits);
+      const int64_t ao = gmap(tab, d.Ab, bb) + gmap(tab, d.Am, m);
+      const int64_t bo = gmap(tab, d.Bb, bb) + gmap(tab, d.Bn, n);
+      for (int64_t k = gl; k < K; k += G) {
+        const C2 a = A[ao + gmap(tab, d.Ak, k)];
+        const C2 b = B[bo + gmap(tab, d.Bk, k)];
+        re = fma((double)a.x, (double)b.x, re);
+        re = fma(-(double)a.y, (double)b.y, re);
+        im = fma((double)a.x, (double)b.y, im);
+        im = fma((double)a.y, (double)b.x, im);
+      }
     }
-    C[o] = C2{re, im};
+    if (G >= 32) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, off);
+        im += __shfl_xor_sync(0xffffffffu, im, off);
+      }
+    }
+    if (G == 128) {
+      if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = re; red[1][threadIdx.x >> 5] = im; }
+      __syncthreads();
+      re = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
+      im = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
+      __syncthreads();
+    }
+    if (o < end && gl == 0) C[o] = C2{(R)re, (R)im};
   }
 }
 

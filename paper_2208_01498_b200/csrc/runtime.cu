@@ -184,9 +184,13 @@ void ensure_gemm_attr() {
 }
 
 // one tensor-core step: pack X, pack Y, GEMM
+constexpr int KC_PER_SPLIT = 4096 / tnd::tc::BK;   // <= 4096 terms per TMEM accumulation
+
 struct TcStep {
   PackDesc px, py;
   int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
+  int64_t p_off = 0;              // split-K partials (arena offset), S > 1 only
+  int S = 1;                      // K splits
   int32_t c_node;
   int nb_bits, m_bits, n_bits, k_bits, BN;
   CUtensorMap ta, tb;
@@ -206,18 +210,41 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
   pack(t.py, t.y_off, t.n_bits);
   if (ev_mid) CK(cudaEventRecord(ev_mid, st));
   dim3 grid((unsigned)(((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN), (unsigned)(((int64_t(1) << t.m_bits) + 127) / 128),
-            (unsigned)(1u << t.nb_bits));
+            (unsigned)((1u << t.nb_bits) * t.S));
+  float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
   if (t.BN == 128) {
     ensure_gemm_attr<128>();
-    tnd::tc::cgemm_bf16x6_kernel<128><<<grid, 128, tnd::tc::Cfg<128>::SMEM, st>>>(
-        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, 0);
+    tnd::tc::cgemm_bf16x6_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
+        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, KC_PER_SPLIT, partial);
   } else {
     ensure_gemm_attr<64>();
-    tnd::tc::cgemm_bf16x6_kernel<64><<<grid, 128, tnd::tc::Cfg<64>::SMEM, st>>>(
-        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, 0);
+    tnd::tc::cgemm_bf16x6_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
+        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, KC_PER_SPLIT, partial);
   }
   g_launches++;
+  if (t.S > 1) {
+    const int64_t n = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+    tnd::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, t.S, n, ptrs_d, t.c_node);
+    g_launches++;
+  }
   CK(cudaGetLastError());
+}
+
+void finish_tc_shape(TcStep& t) {
+  t.BN = (t.n_bits >= 7) ? 128 : 64;
+  const int64_t nk_all = ((int64_t(1) << t.k_bits) + tnd::tc::BK - 1) / tnd::tc::BK;
+  t.S = (int)((nk_all + KC_PER_SPLIT - 1) / KC_PER_SPLIT);
+}
+int64_t tc_partial_bytes(const TcStep& t) {
+  return t.S > 1 ? (int64_t(8) * t.S) << (t.nb_bits + t.m_bits + t.n_bits) : 0;
+}
+
+// threads per output and outputs per CTA of a small step (long reductions split K)
+void set_small_mode(SmallStep& d) {
+  const int ob = d.nb_bits + d.m_bits + d.n_bits;
+  d.g_log2 = (d.k_bits >= 10 && ob <= 12) ? 7 : (d.k_bits >= 6 && ob <= 16) ? 5 : 0;
+  d.opc = (128 >> d.g_log2) * 4;
 }
 
 struct Wave {
@@ -326,7 +353,7 @@ struct tn_plan_s {
         k += 1;
       } else {
         launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
-        k += 3;
+        k += tcs[L.second].S > 1 ? 4 : 3;
       }
     }
     if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
@@ -471,7 +498,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       const auto& fy = swap ? cl.lfree : cl.rfree;
       TcStep t;
       t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
-      t.BN = (t.n_bits >= 7) ? 128 : 64;
+      finish_tc_shape(t);
       t.c_node = c;
       t.px.src = X; t.px.nb_bits = nb; t.px.r_bits = t.m_bits; t.px.k_bits = kk;
       t.px.gb = pool.add(group_of(cl.batch, L[X], l2));
@@ -499,6 +526,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       d.Bb = pool.add(group_of(cl.batch, L[b], l2));
       d.Bk = pool.add(group_of(cl.contr, L[b], l2));
       d.Bn = pool.add(group_of(cl.rfree, L[b], l2));
+      set_small_mode(d);
       small_desc[k] = d;
       L[c].inds = cl.batch;
       L[c].inds.insert(L[c].inds.end(), cl.lfree.begin(), cl.lfree.end());
@@ -550,7 +578,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
         w.prefix.push_back(acc);
         const auto& d = small_desc[k];
         int64_t outs = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
-        acc += (outs + OUTS_PER_CTA - 1) / OUTS_PER_CTA;
+        acc += (outs + d.opc - 1) / d.opc;
         w.steps.push_back(d);
         w.flops += 8.0 * std::ldexp(1.0, d.nb_bits + d.m_bits + d.n_bits + d.k_bits);
         w.bytes += P.esz * (std::ldexp(1.0, L[d.a].bits) + std::ldexp(1.0, L[d.b].bits) + std::ldexp(1.0, L[d.c].bits));
@@ -590,6 +618,11 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     sizes.push_back((int64_t(12) << (t.nb_bits + t.n_bits + t.k_bits)));
     ivs.push_back({step_pos[k], step_pos[k]});
     owner.push_back(-2 - 2 * big_index[k]);
+    if (t.S > 1) {
+      sizes.push_back(tc_partial_bytes(t));
+      ivs.push_back({step_pos[k], step_pos[k]});
+      owner.push_back(-1000000 - big_index[k]);
+    }
   }
   int64_t total = 0;
   auto offs = first_fit(sizes, ivs, total);
@@ -603,6 +636,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   std::vector<void*> ptrs(P.n_nodes, nullptr);
   for (size_t j = 0; j < owner.size(); ++j) {
     if (owner[j] >= 0) ptrs[owner[j]] = P.arena + offs[j];
+    else if (owner[j] <= -1000000) P.tcs[-1000000 - owner[j]].p_off = offs[j];
     else {
       int o = -1 - owner[j];
       if (o % 2 == 0) P.tcs[o / 2].x_off = offs[j];
@@ -1037,7 +1071,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     if (tc) {
       TcStep t;
       t.nb_bits = nb; t.m_bits = mx; t.n_bits = my; t.k_bits = kk;
-      t.BN = my >= 7 ? 128 : 64;
+      finish_tc_shape(t);
       t.c_node = 2;
       t.px.src = 0; t.px.nb_bits = nb; t.px.r_bits = mx; t.px.k_bits = kk;
       t.px.gb = pool.add(group_of(batch, LX, l2)); t.px.gr = pool.add(group_of(g1, LX, l2));
@@ -1046,11 +1080,13 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.py.gb = pool.add(group_of(batch, LY, l2)); t.py.gr = pool.add(group_of(g2, LY, l2));
       t.py.gk = pool.add(group_of(cl.contr, LY, l2));
       size_t xb = size_t(12) << (nb + mx + kk), yb = size_t(12) << (nb + my + kk);
-      char* scratch = (char*)dalloc(xb + yb + 2 * ALIGN);
+      size_t pb = (size_t)tc_partial_bytes(t);
+      char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
       int64_t* tab_d = (int64_t*)dalloc(pool.v.size() * 8);
       h2d(tab_d, pool.v.data(), pool.v.size() * 8);
       t.x_off = 0;
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
+      t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
       t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128);
       t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN);
       launch_tc(t, scratch, ptrs_d, tab_d, st);
@@ -1063,10 +1099,11 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       d.Ak = pool.add(group_of(cl.contr, LX, l2));
       d.Bb = pool.add(group_of(batch, LY, l2)); d.Bk = pool.add(group_of(cl.contr, LY, l2));
       d.Bn = pool.add(group_of(g2, LY, l2));
+      set_small_mode(d);
       Wave w;
       w.steps = {d};
       int64_t outs = int64_t(1) << (nb + mx + my);
-      w.prefix = {0, (outs + OUTS_PER_CTA - 1) / OUTS_PER_CTA};
+      w.prefix = {0, (outs + d.opc - 1) / d.opc};
       w.n_cta = w.prefix[1];
       w.steps_d = (SmallStep*)dalloc(sizeof(SmallStep));
       h2d(w.steps_d, w.steps.data(), sizeof(SmallStep));

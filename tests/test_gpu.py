@@ -2,9 +2,11 @@
 
 Tolerances (DESIGN.md "Tolerances"):
   * step level, complex128 (CUDA-core DFMA): |C - C_ref| <= 1e-12 * sum_k |A||B|
-  * step level, complex64 (bf16x6 tensor cores / fp32 FMA): |C - C_ref| <= 2e-6 * sum_k |A||B|
-    (fp32 storage of A, B contributes 2^-24 relative per product; bf16x6 drops terms
-    below 2^-24; fp32 accumulation adds <= K * 2^-24 in the worst case, ~sqrt(K) typically)
+  * step level, complex64 (bf16x6 tensor cores / fp32 FMA):
+        |C - C_ref| <= (4 + 2 sqrt(K)) 2^-24 * sum_k |A||B|
+    (fp32 storage of A and B: 2 x 2^-24 per product; bf16x6 drops the x_i y_j terms
+    with i + j > 2: < 2 x 2^-24; sequential fp32 accumulation over K terms: a random
+    walk of ~sqrt(K) roundings of 2^-24, with a factor 2 margin)
   * amplitudes: complex128 |a - a_ref| <= 1e-10 * max(|a_ref|, 2^{-n/2});
     complex64 |a - a_ref| <= 1e-5 * max(|a_ref|, 2^{-n/2})  (BASELINE north_star, with the
     RMS amplitude 2^{-n/2} as the scale for amplitudes near zero)
@@ -35,6 +37,10 @@ def _rand(shape, seed, dtype):
     g = np.random.default_rng(seed)
     x = (g.standard_normal(shape) + 1j * g.standard_normal(shape)) / math.sqrt(2)
     return x.astype(np.complex64 if dtype == tb.TN_C64 else np.complex128)
+
+
+def c64_tol(K):
+    return (4.0 + 2.0 * math.sqrt(K)) * 2.0 ** -24
 
 
 def _run_pair(inds_a, inds_b, inds_c, dims, dtype, path, seed=0):
@@ -70,6 +76,8 @@ PAIR_CASES = [
     ([3, 0, 1, 2], [4, 2, 1], [0, 3, 4], [2, 2, 2, 2, 2]),                 # permuted operand layouts
     ([0], [1], [0, 1], [2, 2]),                                            # outer product
     ([0, 1], [0, 1], [], [2, 4]),                                          # full contraction to a scalar
+    (list(range(12)), list(range(12))[::-1], [], [2] * 12),                # K = 4096 -> one CTA per output
+    ([0, 1] + list(range(2, 10)), list(range(2, 10)) + [10], [0, 1, 10], [2] * 11),  # K = 256 -> warp per output
 ]
 
 
@@ -78,7 +86,8 @@ PAIR_CASES = [
 def test_pair_small_path(case, dtype):
     ia, ib, ic, dims = PAIR_CASES[case]
     got, ref, bound = _run_pair(ia, ib, ic, dims, dtype, tb.TN_PATH_SMALL, seed=case)
-    tol = 2e-6 if dtype == tb.TN_C64 else 1e-12
+    K = int(np.prod([dims[i] for i in ia if i in ib and i not in ic])) if ia else 1
+    tol = c64_tol(K) if dtype == tb.TN_C64 else 1e-12
     assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
 
 
@@ -101,6 +110,8 @@ TC_CASES = [
     (0, 9, 8, 9, None),       # 4 x 2 tiles, K = 512 (16 stages)
     (2, 7, 6, 5, 3),          # batch 4, permuted layouts folded into the pack
     (0, 10, 10, 12, 5),       # several tiles, K = 4096, permuted
+    (0, 7, 8, 14, None),      # K = 16384: split-K over 4 CTAs + fp64 reduction
+    (1, 6, 7, 13, 7),         # split-K with batch and ragged M
 ]
 
 
@@ -110,14 +121,14 @@ def test_pair_tensor_core_path(case):
     ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
     got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=10 + case)
     err = np.abs(got - ref)
-    assert np.all(err <= 2e-6 * bound + 1e-30), (err / bound).max()
+    assert np.all(err <= c64_tol(2 ** k) * bound + 1e-30), (err / bound).max()
 
 
 def test_pair_tc_matches_small_path():
     ia, ib, ic, dims = _gemm_case(1, 7, 7, 6, 9)
     g1, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=3)
     g2, _, _ = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_SMALL, seed=3)
-    assert np.all(np.abs(g1 - g2) <= 4e-6 * bound + 1e-30)
+    assert np.all(np.abs(g1 - g2) <= 2 * c64_tol(2 ** 6) * bound + 1e-30)
 
 
 # ------------------------------------------------------------------ plans ----
@@ -244,4 +255,4 @@ def test_config1_full_size_biggest_gemm_sampled():
         b_col = Bm[b, :, j].cpu().numpy().astype(np.complex128)
         want = np.dot(a_row, b_col)
         bound = np.dot(np.abs(a_row), np.abs(b_col))
-        assert abs(Cm[b, i, j].item() - want) <= 2e-6 * bound
+        assert abs(Cm[b, i, j].item() - want) <= c64_tol(K_) * bound
