@@ -24,61 +24,120 @@
 namespace tnd {
 
 // ------------------------------------------------------------------- pack ----
+// Fused permutation + split of one operand into the tensor-core layout.
+// The operand's stored order and the matricised order [b][rows][k] are both
+// row-major over power-of-two dimensions, so the permutation is a permutation of the
+// bits of the element index.  One CTA handles a tile of 2^t_bits elements whose bits
+// T contain the source's 5 lowest bits (coalesced 256-byte reads) and the
+// destination's lowest bits (coalesced 16-byte writes); the tile is transposed
+// through shared memory.
 struct PackDesc {
   int32_t src;                      // node id in the pointer table
   int32_t nb_bits, r_bits, k_bits;
-  GroupMap gb, gr, gk;              // element offsets of (batch, row, k) in the source
+  int32_t t_bits;                   // |T|
+  int32_t ld;                       // lowest destination bits inside T (contiguous runs)
+  int32_t tile_bits;                // bits enumerating tiles
+  int32_t pad;
+  int64_t e_src;                    // tab[e_src + e]: source offset of local element e
+  int64_t e_q;                      // tab[e_q + e]: compact destination index of e
+  GroupMap tile_src, tile_dst;      // tile id -> source / destination element offset
+  GroupMap q_hi;                    // (q >> ld) -> destination offset
+  int64_t plane;                    // rows * K: elements per bf16 plane
 };
 
-__device__ __forceinline__ void split3(float x, __nv_bfloat16& p0, __nv_bfloat16& p1, __nv_bfloat16& p2) {
-  p0 = __float2bfloat16_rn(x);
-  float r = x - __bfloat162float(p0);
-  p1 = __float2bfloat16_rn(r);
-  r = r - __bfloat162float(p1);
-  p2 = __float2bfloat16_rn(r);
+constexpr int PACK_MAX_T = 11;
+constexpr int PACK_THREADS = 256;
+constexpr int PACK_PER_THREAD = (1 << PACK_MAX_T) / PACK_THREADS;   // 8
+
+// smem slot of compact destination index q: XOR-swizzle bits 1-3 by higher bits so the
+// scattered 8-byte stores of phase 1 spread over banks; pairs (bit 0) stay adjacent
+// for the 16-byte loads of phase 2.
+__device__ __forceinline__ int pack_slot(int q) { return q ^ ((((q >> 4) ^ (q >> 7) ^ (q >> 10)) & 7) << 1); }
+
+// split 2 floats into 3 bf16x2 pieces (each the bf16 rounding of the remainder)
+__device__ __forceinline__ void split3x2(float a, float b, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  p0 = *reinterpret_cast<uint32_t*>(&h);
+  float ra = a - __low2float(h), rb = b - __high2float(h);
+  h = __floats2bfloat162_rn(ra, rb);
+  p1 = *reinterpret_cast<uint32_t*>(&h);
+  ra = ra - __low2float(h);
+  rb = rb - __high2float(h);
+  h = __floats2bfloat162_rn(ra, rb);
+  p2 = *reinterpret_cast<uint32_t*>(&h);
 }
 
-// out: 6 planes (piece * 2 + {re, im}) of [b][r][k] bf16; each thread packs 8
-// consecutive k of one (b, r) row: 8 complex loads, 6 x 16-byte stores.
-__global__ void __launch_bounds__(256) pack_bf16x3_kernel(const void* const* __restrict__ ptrs, PackDesc d,
-                                                          const int64_t* __restrict__ tab,
-                                                          __nv_bfloat16* __restrict__ out) {
+// out planes, layout [b][plane][r][k] bf16, plane = 2 * piece + {0: re, 1: im}.
+// Tiles have 2^t_bits elements, 3 <= t_bits <= PACK_MAX_T (11 unless the operand is smaller).
+__global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+                                                                   const int64_t* __restrict__ tab,
+                                                                   __nv_bfloat16* __restrict__ out) {
+  __shared__ __align__(16) float2 s[1 << PACK_MAX_T];
   const float2* __restrict__ src = reinterpret_cast<const float2*>(ptrs[d.src]);
-  const int64_t plane = int64_t(1) << (d.nb_bits + d.r_bits + d.k_bits);
-  const int64_t nvec = plane >> 3;
-  const int64_t kmask8 = (int64_t(1) << (d.k_bits - 3)) - 1;
-  const int64_t rmask = (int64_t(1) << d.r_bits) - 1;
-  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nvec; v += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t k0 = (v & kmask8) << 3;
-    const int64_t row = (v >> (d.k_bits - 3)) & rmask;
-    const int64_t b = v >> (d.k_bits - 3 + d.r_bits);
-    const int64_t base = gmap(tab, d.gb, b) + gmap(tab, d.gr, row);
-    __align__(16) __nv_bfloat16 pc[6][8];
+  const int64_t n_tiles = int64_t(1) << d.tile_bits;
+  const int64_t lmask = (int64_t(1) << d.ld) - 1;
+  const int T = 1 << d.t_bits;
+  // tile-independent local offsets, cached in registers
+  int64_t so[PACK_PER_THREAD];
+  int sl[PACK_PER_THREAD];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float2 x = src[base + gmap(tab, d.gk, k0 + j)];
-      split3(x.x, pc[0][j], pc[2][j], pc[4][j]);
-      split3(x.y, pc[1][j], pc[3][j], pc[5][j]);
+  for (int i = 0; i < PACK_PER_THREAD; ++i) {
+    const int e = threadIdx.x + i * PACK_THREADS;
+    so[i] = e < T ? __ldg(tab + d.e_src + e) : 0;
+    sl[i] = e < T ? pack_slot((int)__ldg(tab + d.e_q + e)) : 0;
+  }
+  const int q0 = threadIdx.x * 8;                       // this thread's 8 destination elements
+  const bool writer = q0 < T;
+  const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t sb = gmap(tab, d.tile_src, tile);
+    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
+    float2 v[PACK_PER_THREAD];
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) v[i] = __ldg(src + sb + so[i]);
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
+    __syncthreads();
+    float4 w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = writer ? *reinterpret_cast<const float4*>(&s[pack_slot(q0 + 2 * j)]) : float4{};
+    __syncthreads();
+    if (!writer) continue;
+    // w[j] = (re_{2j}, im_{2j}, re_{2j+1}, im_{2j+1}); slots of a pair are adjacent
+    uint4 o[6];
+    uint32_t* op = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t r0, r1, r2, i0, i1, i2;
+      split3x2(w[j].x, w[j].z, r0, r1, r2);
+      split3x2(w[j].y, w[j].w, i0, i1, i2);
+      op[0 * 4 + j] = r0; op[1 * 4 + j] = i0; op[2 * 4 + j] = r1;
+      op[3 * 4 + j] = i1; op[4 * 4 + j] = r2; op[5 * 4 + j] = i2;
     }
 #pragma unroll
-    for (int p = 0; p < 6; ++p)
-      *reinterpret_cast<uint4*>(out + p * plane + (v << 3)) = *reinterpret_cast<const uint4*>(pc[p]);
+    for (int p = 0; p < 6; ++p) *reinterpret_cast<uint4*>(out + db + p * d.plane) = o[p];
   }
 }
 
 // ------------------------------------------------------------- tcgen05 -------
 namespace tc {
 
-constexpr int BM = 128;   // rows per tile (TMEM lanes)
-constexpr int BK = 32;    // bf16 elements of K per stage (64-byte rows, SWIZZLE_64B)
+constexpr int BM = 128;    // rows per tile (TMEM lanes)
+constexpr int BK = 32;     // bf16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
+constexpr int PROMO = 1;   // smem stages accumulated per TMEM buffer before promotion
+constexpr int GROUP_M = 8; // CTA rasterization: 8 M-tiles share each B panel in flight
 
 template <int BN>
 struct Cfg {
-  static constexpr int A_PLANE = BM * BK * 2;
+  static constexpr int A_PLANE = BM * BK * 2;              // one bf16 plane tile
   static constexpr int B_PLANE = BN * BK * 2;
-  static constexpr int STAGE = 6 * A_PLANE + 6 * B_PLANE;
+  static constexpr int A_BYTES = 6 * A_PLANE;              // 3 pieces x (re, im)
+  static constexpr int B_BYTES = 6 * B_PLANE;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (3 * STAGE + 2048 <= 227 * 1024) ? 3 : 2;
-  static constexpr int ACC_COLS = 2 * BN;                  // re + im of one accumulator buffer
+  static constexpr int ACC_COLS = 2 * BN;                  // [re | im] of one accumulator buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS;           // ping-pong buffers
   static constexpr int EPI_WARPS = 4 * (BN / 64);          // each owns 32 rows x 64 columns
   static constexpr int THREADS = 32 * (EPI_WARPS + 2);     // + TMA warp + MMA warp
@@ -145,10 +204,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 // Precision: the tensor core's fp32 accumulation
-// truncates, so an accumulator updated T times drifts by ~T/4 ulp toward zero.  Each
-// 32-wide K stage is therefore accumulated in a fresh TMEM buffer (24 MMA updates per
-// element) and promoted by the epilogue warps into fp32 registers with round-to-
-// nearest adds; two TMEM buffers ping-pong so promotion overlaps the next stage.
+// truncates, so an accumulator updated T times drifts by ~T/4 ulp toward zero.  Every
+// 32 elements of K (one smem stage) are therefore accumulated in a fresh TMEM buffer
+// (24 MMA updates per element) and promoted by the epilogue warps into fp32 registers
+// with round-to-nearest adds; two TMEM buffers ping-pong so promotion overlaps the
+// next MMAs.  (A variant with one m128 x n256 MMA over stacked [Br; Bi] / [-Bi; Br]
+// tiles cut shared-memory operand traffic by 25% but needed 32-byte TMA rows and ran
+// slower; the kernel is at the power-capped bf16 throughput anyway -- DESIGN.md.)
 template <int BN>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_bf16x6_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -165,11 +227,20 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TMA_WARP = CF::EPI_WARPS, MMA_WARP = CF::EPI_WARPS + 1;
+  // tile rasterization: groups of GROUP_M M-tiles sweep the N-tiles together (L2 reuse)
+  const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int group = pid / (GROUP_M * n_tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gm = min(n_tiles_m - first_m, GROUP_M);
+  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
+  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
   // split-K: blockIdx.z = split * nb + batch; this CTA covers K chunks [kc0, kc0 + nk)
-  const int n_blk = blockIdx.x, m_blk = blockIdx.y, b = blockIdx.z % nb, split = blockIdx.z / nb;
+  const int b = blockIdx.z % nb, split = blockIdx.z / nb;
   const int nk_all = (K + BK - 1) / BK;
   const int kc0 = split * kc_per_split;
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+  const int n_promo = (nk + PROMO - 1) / PROMO;
 
   if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -196,10 +267,8 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], CF::STAGE);
         uint8_t* st = smem + s * CF::STAGE;
-        for (int p = 0; p < 6; ++p)
-          tma_load_3d(&tmA, st + p * CF::A_PLANE, &full[s], (kc0 + kc) * BK, m_blk * BM, p * nb + b);
-        for (int p = 0; p < 6; ++p)
-          tma_load_3d(&tmB, st + 6 * CF::A_PLANE + p * CF::B_PLANE, &full[s], (kc0 + kc) * BK, n_blk * BN, p * nb + b);
+        tma_load_3d(&tmA, st, &full[s], (kc0 + kc) * BK, m_blk * BM, b * 6);               // 6 planes
+        tma_load_3d(&tmB, st + CF::A_BYTES, &full[s], (kc0 + kc) * BK, n_blk * BN, b * 6); // 6 planes
       }
     }
   } else if (warp == MMA_WARP) {
@@ -212,9 +281,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % CF::STAGES;
         const uint32_t ph = (kc / CF::STAGES) & 1;
-        const int buf = kc & 1;
-        const uint32_t tph = (kc >> 1) & 1;
-        mbar_wait(&tempty[buf], tph ^ 1);       // epilogue has drained this buffer
+        const int pi = kc / PROMO;
+        const int buf = pi & 1;
+        const bool first = (kc % PROMO) == 0;
+        const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
+        if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // epilogue drained this buffer
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
@@ -225,17 +296,17 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
           for (int q = 0; q < 6; ++q) {
             const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
             const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
-            const uint64_t b_re = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint64_t b_im = make_desc_sw64(st + 6 * CF::A_PLANE + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint32_t acc = (ks | q) != 0;   // fresh accumulator every stage
+            const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;   // fresh accumulator per promotion
             mma_bf16(t_re, a_re, b_re, idesc, acc);
-            mma_bf16(t_re, a_im, b_im, idesc_negA, 1);
+            mma_bf16(t_re, a_im, b_im, idesc_negA, 1u);
             mma_bf16(t_im, a_re, b_im, idesc, acc);
-            mma_bf16(t_im, a_im, b_re, idesc, 1);
+            mma_bf16(t_im, a_im, b_re, idesc, 1u);
           }
         }
-        mma_commit(&empty[s]);     // smem stage free once these MMAs have read it
-        mma_commit(&tfull[buf]);   // accumulator buffer ready for promotion
+        mma_commit(&empty[s]);                 // smem stage free once these MMAs have read it
+        if (last) mma_commit(&tfull[buf]);     // accumulator buffer ready for promotion
       }
     }
   } else {
@@ -246,9 +317,9 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     float ar[64], ai[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
-    for (int kc = 0; kc < nk; ++kc) {
-      const int buf = kc & 1;
-      const uint32_t tph = (kc >> 1) & 1;
+    for (int pi = 0; pi < n_promo; ++pi) {
+      const int buf = pi & 1;
+      const uint32_t tph = (pi >> 1) & 1;
       mbar_wait(&tfull[buf], tph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;

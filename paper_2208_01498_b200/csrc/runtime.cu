@@ -160,11 +160,12 @@ EncodeFn encode_fn() {
   }
   return fn;
 }
-CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int box_rows) {
+// packed operand planes [b][plane][rows][K] bf16; a box = BK x box_rows x all planes
+CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int box_rows, int planes) {
   CUtensorMap m;
-  cuuint64_t dims[3] = {cuuint64_t(1) << k_bits, cuuint64_t(1) << r_bits, cuuint64_t(6) << nb_bits};
+  cuuint64_t dims[3] = {cuuint64_t(1) << k_bits, cuuint64_t(1) << r_bits, cuuint64_t(planes) << nb_bits};
   cuuint64_t strides[2] = {(cuuint64_t(1) << k_bits) * 2, (cuuint64_t(1) << (k_bits + r_bits)) * 2};
-  cuuint32_t box[3] = {(cuuint32_t)tnd::tc::BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)tnd::tc::BK, (cuuint32_t)box_rows, (cuuint32_t)planes};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -199,18 +200,17 @@ struct TcStep {
 
 void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                cudaEvent_t ev_mid = nullptr) {
-  auto pack = [&](const PackDesc& d, int64_t off, int r_bits) {
-    const int64_t nvec = (int64_t(1) << (d.nb_bits + r_bits + d.k_bits)) >> 3;
-    const int64_t blocks = std::min<int64_t>((nvec + 255) / 256, 148 * 64);
-    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, 256, 0, st>>>(ptrs_d, d, tab_d,
+  auto pack = [&](const PackDesc& d, int64_t off, int) {
+    const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
+    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(ptrs_d, d, tab_d,
                                                               reinterpret_cast<__nv_bfloat16*>(arena + off));
     g_launches++;
   };
   pack(t.px, t.x_off, t.m_bits);
   pack(t.py, t.y_off, t.n_bits);
   if (ev_mid) CK(cudaEventRecord(ev_mid, st));
-  dim3 grid((unsigned)(((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN), (unsigned)(((int64_t(1) << t.m_bits) + 127) / 128),
-            (unsigned)((1u << t.nb_bits) * t.S));
+  const int64_t tiles = (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN) * (((int64_t(1) << t.m_bits) + 127) / 128);
+  dim3 grid((unsigned)tiles, 1, (unsigned)((1u << t.nb_bits) * t.S));
   float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
   if (t.BN == 128) {
     ensure_gemm_attr<128>();
@@ -262,6 +262,79 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
                                                                      ptrs_d, OUTS_PER_CTA);
   g_launches++;
   CK(cudaGetLastError());
+}
+
+// Pack descriptor: bit permutation from the operand's stored layout to [b][rows][k]
+// (destination planes [b][6][rows][k]); see pack_bf16x3_kernel.
+PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
+                   const std::vector<int>& rows, const std::vector<int>& kg, const std::vector<int>& l2) {
+  PackDesc d{};
+  d.src = src_node;
+  d.nb_bits = sum_bits(batch, l2);
+  d.r_bits = sum_bits(rows, l2);
+  d.k_bits = sum_bits(kg, l2);
+  const int D = d.nb_bits + d.r_bits + d.k_bits, RK = d.r_bits + d.k_bits;
+  d.plane = int64_t(1) << RK;
+  // source bit of every destination bit
+  std::map<int, int> src_shift;
+  {
+    int sh = 0;
+    for (int k = (int)L.inds.size() - 1; k >= 0; --k) { src_shift[L.inds[k]] = sh; sh += l2[L.inds[k]]; }
+  }
+  std::vector<int> order = batch;
+  order.insert(order.end(), rows.begin(), rows.end());
+  order.insert(order.end(), kg.begin(), kg.end());
+  std::vector<int> pi(D);
+  {
+    int sh = 0;
+    for (int k = (int)order.size() - 1; k >= 0; --k) {
+      int i = order[k];
+      for (int u = 0; u < l2[i]; ++u) pi[sh + u] = src_shift.at(i) + u;
+      sh += l2[i];
+    }
+  }
+  auto dst_contrib = [&](int dbit) -> int64_t {
+    return dbit < RK ? (int64_t(1) << dbit) : ((int64_t(1) << (dbit - RK)) * 6 * d.plane);
+  };
+  std::vector<char> inT(D, 0);
+  int t = 0;
+  for (int j = 0; j < std::min(6, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
+  for (int j = 0; j < D; ++j) if (pi[j] < 5 && !inT[j]) { inT[j] = 1; ++t; }
+  for (int j = 0; j < D && t < std::min(tnd::PACK_MAX_T, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
+  if (t < 3) throw Err(TN_EUNSUPPORTED, "pack needs >= 8 elements per operand");
+  d.t_bits = t;
+  int ld = 0;
+  while (ld < D && inT[ld]) ++ld;
+  d.ld = std::min(ld, RK);
+  std::vector<int> Tsrc, Tdst, nonT;
+  for (int j = 0; j < D; ++j) (inT[j] ? Tdst : nonT).push_back(j);
+  Tsrc = Tdst;
+  std::sort(Tsrc.begin(), Tsrc.end(), [&](int a, int b) { return pi[a] < pi[b]; });
+  std::map<int, int> rank;
+  for (size_t k = 0; k < Tdst.size(); ++k) rank[Tdst[k]] = (int)k;
+  d.e_src = (int64_t)pool.v.size();
+  for (int64_t e = 0; e < (int64_t(1) << t); ++e) {
+    int64_t o = 0;
+    for (int i = 0; i < t; ++i) if ((e >> i) & 1) o += int64_t(1) << pi[Tsrc[i]];
+    pool.v.push_back(o);
+  }
+  d.e_q = (int64_t)pool.v.size();
+  for (int64_t e = 0; e < (int64_t(1) << t); ++e) {
+    int64_t q = 0;
+    for (int i = 0; i < t; ++i) if ((e >> i) & 1) q |= int64_t(1) << rank[Tsrc[i]];
+    pool.v.push_back(q);
+  }
+  d.tile_bits = (int)nonT.size();
+  std::vector<std::pair<int, int64_t>> gs, gd, gq;
+  for (int k = (int)nonT.size() - 1; k >= 0; --k) {
+    gs.push_back({1, int64_t(1) << pi[nonT[k]]});
+    gd.push_back({1, dst_contrib(nonT[k])});
+  }
+  for (int k = (int)Tdst.size() - 1; k >= d.ld; --k) gq.push_back({1, dst_contrib(Tdst[k])});
+  d.tile_src = pool.add(gs);
+  d.tile_dst = pool.add(gd);
+  d.q_hi = pool.add(gq);
+  return d;
 }
 
 // decide the path of a step (TC only for complex64 GEMM-shaped steps)
@@ -500,14 +573,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
       finish_tc_shape(t);
       t.c_node = c;
-      t.px.src = X; t.px.nb_bits = nb; t.px.r_bits = t.m_bits; t.px.k_bits = kk;
-      t.px.gb = pool.add(group_of(cl.batch, L[X], l2));
-      t.px.gr = pool.add(group_of(fx, L[X], l2));
-      t.px.gk = pool.add(group_of(cl.contr, L[X], l2));
-      t.py.src = Y; t.py.nb_bits = nb; t.py.r_bits = t.n_bits; t.py.k_bits = kk;
-      t.py.gb = pool.add(group_of(cl.batch, L[Y], l2));
-      t.py.gr = pool.add(group_of(fy, L[Y], l2));
-      t.py.gk = pool.add(group_of(cl.contr, L[Y], l2));
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -644,8 +711,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     }
   }
   for (auto& t : P.tcs) {
-    t.ta = make_plane_map(P.arena + t.x_off, t.k_bits, t.m_bits, t.nb_bits, 128);
-    t.tb = make_plane_map(P.arena + t.y_off, t.k_bits, t.n_bits, t.nb_bits, t.BN);
+    t.ta = make_plane_map(P.arena + t.x_off, t.k_bits, t.m_bits, t.nb_bits, 128, 6);
+    t.tb = make_plane_map(P.arena + t.y_off, t.k_bits, t.n_bits, t.nb_bits, t.BN, 6);
   }
 
   // ---- uploads ----
@@ -743,8 +810,8 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
         pr.n_pack += 2;
         pr.n_gemm += 1;
         pr.flops_gemm += t.flops;
-        pr.bytes_pack += (double)P.esz * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
-                                          std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits)) * 2.5;  // read 8 B, write 12 B
+        pr.bytes_pack += 20.0 * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +   // read 8 B, write 12 B
+                                 std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits));
       }
     }
   }
@@ -1073,12 +1140,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.nb_bits = nb; t.m_bits = mx; t.n_bits = my; t.k_bits = kk;
       finish_tc_shape(t);
       t.c_node = 2;
-      t.px.src = 0; t.px.nb_bits = nb; t.px.r_bits = mx; t.px.k_bits = kk;
-      t.px.gb = pool.add(group_of(batch, LX, l2)); t.px.gr = pool.add(group_of(g1, LX, l2));
-      t.px.gk = pool.add(group_of(cl.contr, LX, l2));
-      t.py.src = 1; t.py.nb_bits = nb; t.py.r_bits = my; t.py.k_bits = kk;
-      t.py.gb = pool.add(group_of(batch, LY, l2)); t.py.gr = pool.add(group_of(g2, LY, l2));
-      t.py.gk = pool.add(group_of(cl.contr, LY, l2));
+      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2);
+      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2);
       size_t xb = size_t(12) << (nb + mx + kk), yb = size_t(12) << (nb + my + kk);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
@@ -1087,8 +1150,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.x_off = 0;
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
-      t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128);
-      t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN);
+      t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128, 6);
+      t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN, 6);
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies
     } else {
