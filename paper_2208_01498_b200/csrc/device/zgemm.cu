@@ -1,0 +1,198 @@
+// complex128 GEMM-shaped steps on the FP64 tensor pipe (DMMA).
+//   C[b][m][n] = sum_k A[b][m][k] * B[b][k][n]     (Eq. (3), l.82-86)
+// tcgen05 has no f64 kind; sm_100a's FP64 tensor instructions are mma.sync
+// m16n8k4 f64 (SASS DMMA.8x8x4).  Operands come from the fp64 variant of the tiled
+// transpose pack: 2 planes (re, im) of [b][rows][K]; complex arithmetic is planar,
+// Cr += Ar.Br + (-Ai).Bi, Ci += Ar.Bi + Ai.Br, accumulated in fp64 registers.
+// CTA tile 64 x 64 complex, 4 warps of 32 x 32, K staged 16 at a time through a
+// 2-stage cp.async ring with an XOR swizzle of 16-byte chunks (conflict-free-ish
+// fragment loads).
+#include "common.cuh"
+
+namespace tnd {
+
+// ------------------------------------------------------------- fp64 pack -----
+// Same bit-permutation tiling as pack_bf16x3_kernel (see PackDesc); output planes
+// [b][2][rows][K] complex128 -> (re plane, im plane) of fp64.
+__global__ void __launch_bounds__(PACK_THREADS) pack_f64x2_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+                                                                  const int64_t* __restrict__ tab,
+                                                                  double* __restrict__ out) {
+  __shared__ __align__(16) double2 s[1 << PACK_MAX_T];
+  const double2* __restrict__ src = reinterpret_cast<const double2*>(ptrs[d.src]);
+  const int64_t n_tiles = int64_t(1) << d.tile_bits;
+  const int64_t lmask = (int64_t(1) << d.ld) - 1;
+  const int T = 1 << d.t_bits;
+  int64_t so[PACK_PER_THREAD];
+  int sl[PACK_PER_THREAD];
+#pragma unroll
+  for (int i = 0; i < PACK_PER_THREAD; ++i) {
+    const int e = threadIdx.x + i * PACK_THREADS;
+    so[i] = e < T ? __ldg(tab + d.e_src + e) : 0;
+    sl[i] = e < T ? (int)__ldg(tab + d.e_q + e) : 0;
+  }
+  const int q0 = threadIdx.x * 8;
+  const bool writer = q0 < T;
+  // destination offsets of the packed layout are in units of one fp64 plane element;
+  // the host built tile_dst / q_hi for 2 planes per batch
+  const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t sb = gmap(tab, d.tile_src, tile);
+    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
+    double2 v[PACK_PER_THREAD];
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) v[i] = src[sb + so[i]];
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
+    __syncthreads();
+    double re[8], im[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double2 w = writer ? s[q0 + j] : double2{0.0, 0.0};
+      re[j] = w.x;
+      im[j] = w.y;
+    }
+    __syncthreads();
+    if (!writer) continue;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      *reinterpret_cast<double2*>(out + db + j) = double2{re[j], re[j + 1]};
+      *reinterpret_cast<double2*>(out + db + d.plane + j) = double2{im[j], im[j + 1]};
+    }
+  }
+}
+
+// ------------------------------------------------------------------ DMMA -----
+namespace zg {
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 128, STAGES = 2;
+constexpr int PLANE_TILE = BM * BK;                       // doubles per plane per tile (BM == BN)
+constexpr int STAGE_DOUBLES = 4 * PLANE_TILE;             // A re, A im, B re, B im
+constexpr int SMEM = STAGES * STAGE_DOUBLES * 8;          // 64 KB
+constexpr int GROUP_M = 8;
+
+__device__ __forceinline__ int swz(int row, int col) {      // col in doubles (0..15)
+  return row * BK + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// A planes: [b][2][M][K], B planes: [b][2][N][K] (fp64, K contiguous)
+__global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __restrict__ Ap, const double* __restrict__ Bp,
+                                                             void* const* __restrict__ ptrs, int32_t c_node, int32_t M,
+                                                             int32_t N, int32_t K) {
+  extern __shared__ __align__(16) double sm[];
+  const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int group = pid / (GROUP_M * n_tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gm = min(n_tiles_m - first_m, GROUP_M);
+  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
+  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+  const int b = blockIdx.z;
+  const double* A = Ap + (int64_t)b * 2 * M * (int64_t)K;
+  const double* B = Bp + (int64_t)b * 2 * N * (int64_t)K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+
+  auto load_stage = [&](int stage, int k0) {
+    double* st = sm + stage * STAGE_DOUBLES;
+    // 4 planes x 64 rows x 8 chunks of 16 B = 2048 chunks, 16 per thread
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = threadIdx.x + i * THREADS;
+      const int plane = c >> 9;                  // 0: A re, 1: A im, 2: B re, 3: B im
+      const int row = (c >> 3) & 63;
+      const int ch = c & 7;
+      const bool isA = plane < 2;
+      const int grow = (isA ? m_blk * BM : n_blk * BN) + row;
+      const int gk = k0 + ch * 2;
+      const bool valid = grow < (isA ? M : N) && gk < K;
+      const double* base = isA ? A + (int64_t)(plane & 1) * M * K : B + (int64_t)(plane & 1) * N * K;
+      const double* src = valid ? base + (int64_t)grow * K + gk : base;
+      cp_async16(st + plane * PLANE_TILE + row * BK + ((ch ^ (row & 7)) << 1), src, valid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  double cr[2][4][4], ci[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { cr[i][j][r] = 0.0; ci[i][j][r] = 0.0; }
+
+  const int nk = (K + BK - 1) / BK;
+  load_stage(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      load_stage((kc + 1) & 1, (kc + 1) * BK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* st = sm + (kc & 1) * STAGE_DOUBLES;
+    const double* sAr = st;
+    const double* sAi = st + PLANE_TILE;
+    const double* sBr = st + 2 * PLANE_TILE;
+    const double* sBi = st + 3 * PLANE_TILE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r0 = wm + i * 16 + g;
+        ar[i][0] = sAr[swz(r0, kk + t)];
+        ar[i][1] = sAr[swz(r0 + 8, kk + t)];
+        ai[i][0] = sAi[swz(r0, kk + t)];
+        ai[i][1] = sAi[swz(r0 + 8, kk + t)];
+        nai[i][0] = -ai[i][0];
+        nai[i][1] = -ai[i][1];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n0 = wn + j * 8 + g;
+        br[j] = sBr[swz(n0, kk + t)];
+        bi[j] = sBi[swz(n0, kk + t)];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
+          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
+          dmma(ci[i][j], ar[i][0], ar[i][1], bi[j]);
+          dmma(ci[i][j], ai[i][0], ai[i][1], br[j]);
+        }
+    }
+    __syncthreads();
+  }
+  double2* C = reinterpret_cast<double2*>(ptrs[c_node]) + (int64_t)b * M * (int64_t)N;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = m_blk * BM + wm + i * 16 + g + 8 * h;
+        const int col = n_blk * BN + wn + j * 8 + 2 * t;
+        if (row < M && col < N) {
+          double2* cp = C + (int64_t)row * N + col;
+          cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
+          if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
+        }
+      }
+}
+}  // namespace zg
+}  // namespace tnd

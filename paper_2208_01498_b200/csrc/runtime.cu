@@ -29,6 +29,7 @@
 #include "device/common.cuh"
 #include "device/gemm_tc.cu"
 #include "device/small.cu"
+#include "device/zgemm.cu"
 #include "host/tn_host.hpp"
 #include "tn.h"
 
@@ -188,6 +189,7 @@ void ensure_gemm_attr() {
 constexpr int KC_PER_SPLIT = 4096 / tnd::tc::BK;   // <= 4096 terms per TMEM accumulation
 
 struct TcStep {
+  int kind = 0;                   // 0: complex64 bf16x6 tcgen05; 1: complex128 DMMA
   PackDesc px, py;
   int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
   int64_t p_off = 0;              // split-K partials (arena offset), S > 1 only
@@ -198,8 +200,33 @@ struct TcStep {
   double flops;
 };
 
+void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
+                 cudaEvent_t ev_mid) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tnd::zg::zgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tnd::zg::SMEM));
+    attr = true;
+  }
+  for (const PackDesc* d : {&t.px, &t.py}) {
+    const int64_t blocks = std::min<int64_t>(int64_t(1) << d->tile_bits, 148 * 8);
+    tnd::pack_f64x2_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
+        ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)));
+    g_launches++;
+  }
+  if (ev_mid) CK(cudaEventRecord(ev_mid, st));
+  const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
+                        (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
+  dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
+  tnd::zg::zgemm_dmma_kernel<<<grid, tnd::zg::THREADS, tnd::zg::SMEM, st>>>(
+      reinterpret_cast<const double*>(arena + t.x_off), reinterpret_cast<const double*>(arena + t.y_off), ptrs_d,
+      t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
 void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                cudaEvent_t ev_mid = nullptr) {
+  if (t.kind == 1) return launch_dmma(t, arena, ptrs_d, tab_d, st, ev_mid);
   auto pack = [&](const PackDesc& d, int64_t off, int) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
     tnd::pack_bf16x3_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(ptrs_d, d, tab_d,
@@ -267,7 +294,8 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
 // Pack descriptor: bit permutation from the operand's stored layout to [b][rows][k]
 // (destination planes [b][6][rows][k]); see pack_bf16x3_kernel.
 PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
-                   const std::vector<int>& rows, const std::vector<int>& kg, const std::vector<int>& l2) {
+                   const std::vector<int>& rows, const std::vector<int>& kg, const std::vector<int>& l2,
+                   int planes = 6) {
   PackDesc d{};
   d.src = src_node;
   d.nb_bits = sum_bits(batch, l2);
@@ -294,7 +322,7 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
     }
   }
   auto dst_contrib = [&](int dbit) -> int64_t {
-    return dbit < RK ? (int64_t(1) << dbit) : ((int64_t(1) << (dbit - RK)) * 6 * d.plane);
+    return dbit < RK ? (int64_t(1) << dbit) : ((int64_t(1) << (dbit - RK)) * planes * d.plane);
   };
   std::vector<char> inT(D, 0);
   int t = 0;
@@ -339,8 +367,16 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
 
 // decide the path of a step (TC only for complex64 GEMM-shaped steps)
 bool want_tc(int dtype, int nb, int m, int n, int k) {
-  if (dtype != TN_C64) return false;
+  if (dtype == TN_C128)   // DMMA tiles of 64 x 64 complex, K staged 16 at a time
+    return k >= 3 && std::max(m, n) >= 6 && std::min(m, n) >= 5 && (nb + m + n + k) >= 20;
   return k >= 4 && std::max(m, n) >= 6 && std::min(m, n) >= 4 && (nb + m + n + k) >= 22;
+}
+void finish_tc_kind(TcStep& t, int dtype) {
+  t.kind = dtype == TN_C128 ? 1 : 0;
+  if (t.kind == 1) { t.S = 1; t.BN = tnd::zg::BN; }
+}
+int64_t pack_bytes(const TcStep& t, int rows_bits) {
+  return (t.kind == 1 ? int64_t(16) : int64_t(12)) << (t.nb_bits + rows_bits + t.k_bits);
 }
 
 // first-fit offsets for (size, [lo, hi]) items
@@ -573,8 +609,9 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
       finish_tc_shape(t);
       t.c_node = c;
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2);
-      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2);
+      finish_tc_kind(t, P.dtype);
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 6);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 6);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -679,10 +716,10 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   for (size_t k = 0; k < ord.steps.size(); ++k) {
     if (!kind[k]) continue;
     const auto& t = P.tcs[big_index[k]];
-    sizes.push_back((int64_t(12) << (t.nb_bits + t.m_bits + t.k_bits)));
+    sizes.push_back(pack_bytes(t, t.m_bits));
     ivs.push_back({step_pos[k], step_pos[k]});
     owner.push_back(-1 - 2 * big_index[k]);
-    sizes.push_back((int64_t(12) << (t.nb_bits + t.n_bits + t.k_bits)));
+    sizes.push_back(pack_bytes(t, t.n_bits));
     ivs.push_back({step_pos[k], step_pos[k]});
     owner.push_back(-2 - 2 * big_index[k]);
     if (t.S > 1) {
@@ -711,6 +748,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     }
   }
   for (auto& t : P.tcs) {
+    if (t.kind == 1) continue;
     t.ta = make_plane_map(P.arena + t.x_off, t.k_bits, t.m_bits, t.nb_bits, 128, 6);
     t.tb = make_plane_map(P.arena + t.y_off, t.k_bits, t.n_bits, t.nb_bits, t.BN, 6);
   }
@@ -1114,7 +1152,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     const NodeLayout& LY = l_first ? LB : LA;
     int mx = sum_bits(g1, l2), my = sum_bits(g2, l2);
     bool tc = path == TN_PATH_TC || (path == TN_PATH_AUTO && want_tc(dtype, nb, mx, my, kk));
-    if (tc && (dtype != TN_C64 || kk < 4)) throw Err(TN_EUNSUPPORTED, "tensor-core path needs complex64 and K >= 16");
+    if (tc && kk < (dtype == TN_C64 ? 4 : 1)) throw Err(TN_EUNSUPPORTED, "tensor-core path needs K >= 16 (complex64) / 2 (complex128)");
     cudaStream_t st = (cudaStream_t)stream;
     int cur = 0;
     CK(cudaGetDevice(&cur));
@@ -1139,10 +1177,11 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       TcStep t;
       t.nb_bits = nb; t.m_bits = mx; t.n_bits = my; t.k_bits = kk;
       finish_tc_shape(t);
+      finish_tc_kind(t, dtype);
       t.c_node = 2;
-      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2);
-      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2);
-      size_t xb = size_t(12) << (nb + mx + kk), yb = size_t(12) << (nb + my + kk);
+      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 6);
+      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 6);
+      size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
       int64_t* tab_d = (int64_t*)dalloc(pool.v.size() * 8);
@@ -1150,8 +1189,10 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.x_off = 0;
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
-      t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128, 6);
-      t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN, 6);
+      if (t.kind == 0) {
+        t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128, 6);
+        t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN, 6);
+      }
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies
     } else {

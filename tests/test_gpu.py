@@ -124,6 +124,22 @@ def test_pair_tensor_core_path(case):
     assert np.all(err <= c64_tol(2 ** k) * bound + 1e-30), (err / bound).max()
 
 
+DMMA_CASES = [
+    (0, 6, 6, 4, None),       # one 64x64 tile, K = 16
+    (0, 5, 7, 3, 2),          # ragged M = 32, N = 128, K = 8, permuted
+    (2, 7, 6, 9, 4),          # batch 4, K = 512 (32 stages), permuted
+    (0, 9, 9, 6, None),       # 64 tiles
+]
+
+
+@pytest.mark.parametrize("case", range(len(DMMA_CASES)))
+def test_pair_complex128_dmma_path(case):
+    nb, m, n, k, ps = DMMA_CASES[case]
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
+    assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
+
+
 def test_pair_tc_matches_small_path():
     ia, ib, ic, dims = _gemm_case(1, 7, 7, 6, 9)
     g1, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=3)
@@ -219,6 +235,15 @@ def test_contract_device_accumulates_on_device():
     plan.contract_device(bits.data_ptr(), 0, 1, amp.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert abs(amp.item() - 2 * plan.contract(x)) < 1e-13
+
+
+@pytest.mark.slow
+def test_config3_full_size_sampled_amplitudes():
+    """configs[3] (IQP 10x10, r = 2, complex128, hyperedges): plan at full size; two of
+    the 256 seeded amplitudes against the oracle along its (bit-identical) order."""
+    c = config_circuit(3)
+    plan = _plan_vs_oracle(c, tb.TN_C128, seed=0, hyper=True, n_bits=1, with_zero=False)
+    assert plan.info()["n_steps_tc"] >= 1
 
 
 # ------------------------------------------------ full-size config 1 ------
