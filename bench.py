@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "contraction FLOP/s"
 CONFIG_IDX = 1
-SLICE_LOG2 = 31          # largest tensor of a slice: 2^31 complex64 = 16 GB
+SLICE_LOGS = (32, 31)    # largest tensor of a slice: 2^32 complex64 = 32 GB (arena ~160 GB), else 2^31
 ORDER_SEED = 0
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # split-precision complex64: one complex MAC = 4 real products x 6 bf16 piece products
@@ -102,7 +102,7 @@ def workload():
     return c, bits
 
 
-def cpu_baseline_sample(c, bits, budget_s=15.0):
+def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=SLICE_LOGS[0]):
     """The oracle as it stands on the host cores: slice 0 of bitstring 0 of the same
     network/order (oracle.ssa.find_order + choose_slices), contracting the steps of
     the separator tree in order with oracle.contract.contract_pair until `budget_s`
@@ -117,7 +117,7 @@ def cpu_baseline_sample(c, bits, budget_s=15.0):
         cores = os.cpu_count()
     net = build_network(c)
     steps, _ = find_order(net, seed=ORDER_SEED)
-    sl = choose_slices(net, steps, SLICE_LOG2)
+    sl = choose_slices(net, steps, slice_log2)
     kept = kept_per_step(net, steps)
     fixed = {i: 0 for i in sl}
     n = len(net.tensors)
@@ -184,8 +184,16 @@ def run_ours(args):
 
     c, bits = workload()
     net = tb.Network.from_circuit(c)
-    order = tb.Order(net, seed=ORDER_SEED, max_log2_size=SLICE_LOG2)
-    plan = tb.Plan(net, order, dtype=tb.TN_C64, device=local)
+    plan = None
+    for slice_log2 in SLICE_LOGS:
+        order = tb.Order(net, seed=ORDER_SEED, max_log2_size=slice_log2)
+        try:
+            plan = tb.Plan(net, order, dtype=tb.TN_C64, device=local)
+            break
+        except tb.TnError as e:       # arena does not fit this GPU: slice further
+            print(f"slicing target 2^{slice_log2}: {e}", file=sys.stderr)
+    if plan is None:
+        raise RuntimeError("no slicing target fits device memory")
     pinfo = plan.info()
     n_slices = int(pinfo["n_slices"])
     flops_slice = float(pinfo["flops_per_slice"])
@@ -274,7 +282,7 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget, slice_log2=slice_log2)
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()

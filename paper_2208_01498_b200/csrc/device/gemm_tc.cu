@@ -71,9 +71,9 @@ __device__ __forceinline__ void split3x2(float a, float b, uint32_t& p0, uint32_
 // Tiles have 2^t_bits elements, 3 <= t_bits <= PACK_MAX_T (11 unless the operand is smaller).
 __global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
-                                                                   __nv_bfloat16* __restrict__ out) {
+                                                                   __nv_bfloat16* __restrict__ out, int64_t src_base) {
   __shared__ __align__(16) float2 s[1 << PACK_MAX_T];
-  const float2* __restrict__ src = reinterpret_cast<const float2*>(ptrs[d.src]);
+  const float2* __restrict__ src = reinterpret_cast<const float2*>(ptrs[d.src]) + src_base;
   const int64_t n_tiles = int64_t(1) << d.tile_bits;
   const int64_t lmask = (int64_t(1) << d.ld) - 1;
   const int T = 1 << d.t_bits;
@@ -215,7 +215,7 @@ template <int BN>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_bf16x6_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
-                        int32_t nb, int32_t kc_per_split, float2* __restrict__ partial) {
+                        int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate) {
   using CF = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -345,6 +345,13 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     const int col0 = n_blk * BN + ch * 64;
     if (row < M && col0 < N) {
       float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
+      if (accumulate && !partial) {        // K-slab > 0: C += this slab's product
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          ar[j] += (j < N - col0) ? crow[j].x : 0.f;
+          ai[j] += (j < N - col0) ? crow[j].y : 0.f;
+        }
+      }
       if (N - col0 >= 64) {
 #pragma unroll
         for (int j = 0; j < 64; j += 2) *reinterpret_cast<float4*>(crow + j) = make_float4(ar[j], ai[j], ar[j + 1], ai[j + 1]);
@@ -364,10 +371,16 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 
 // C[i] = sum_s partial[s][i], summed in fp64 (split-K epilogue)
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float2* __restrict__ partial, int32_t S,
-                                                            int64_t n, void* const* __restrict__ ptrs, int32_t c_node) {
+                                                            int64_t n, void* const* __restrict__ ptrs, int32_t c_node,
+                                                            int32_t accumulate) {
   float2* C = reinterpret_cast<float2*>(ptrs[c_node]);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double re = 0.0, im = 0.0;
+    if (accumulate) {
+      const float2 c = C[i];
+      re = c.x;
+      im = c.y;
+    }
     for (int s = 0; s < S; ++s) {
       const float2 v = partial[(int64_t)s * n + i];
       re += v.x;

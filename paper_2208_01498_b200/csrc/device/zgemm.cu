@@ -16,9 +16,9 @@ namespace tnd {
 // [b][2][rows][K] complex128 -> (re plane, im plane) of fp64.
 __global__ void __launch_bounds__(PACK_THREADS) pack_f64x2_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                   const int64_t* __restrict__ tab,
-                                                                  double* __restrict__ out) {
+                                                                  double* __restrict__ out, int64_t src_base) {
   __shared__ __align__(16) double2 s[1 << PACK_MAX_T];
-  const double2* __restrict__ src = reinterpret_cast<const double2*>(ptrs[d.src]);
+  const double2* __restrict__ src = reinterpret_cast<const double2*>(ptrs[d.src]) + src_base;
   const int64_t n_tiles = int64_t(1) << d.tile_bits;
   const int64_t lmask = (int64_t(1) << d.ld) - 1;
   const int T = 1 << d.t_bits;

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -193,27 +194,43 @@ struct TcStep {
   PackDesc px, py;
   int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
   int64_t p_off = 0;              // split-K partials (arena offset), S > 1 only
-  int S = 1;                      // K splits
+  int S = 1;                      // K splits per slab
+  int k_lo = 0;                   // log2 K of one slab
+  int n_slabs = 1;                // K-slabs packed and multiplied in turn (bounded pack buffers)
+  std::vector<int64_t> slab_x, slab_y;   // source offsets of each slab
   int32_t c_node;
   int nb_bits, m_bits, n_bits, k_bits, BN;
   CUtensorMap ta, tb;
   double flops;
 };
 
+// profiling marks: an event recorded before each kernel class (0 small, 1 pack, 2 gemm,
+// 3 reduce, 4 other); time between consecutive marks is attributed to the earlier one
+struct Marks {
+  std::vector<std::pair<cudaEvent_t, int>> v;
+  void mark(cudaStream_t st, int cat) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, st));
+    v.push_back({e, cat});
+  }
+};
+
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
-                 cudaEvent_t ev_mid) {
+                 Marks* mk) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(tnd::zg::zgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tnd::zg::SMEM));
     attr = true;
   }
+  if (mk) mk->mark(st, 1);
   for (const PackDesc* d : {&t.px, &t.py}) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d->tile_bits, 148 * 8);
     tnd::pack_f64x2_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
-        ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)));
+        ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)), 0);
     g_launches++;
   }
-  if (ev_mid) CK(cudaEventRecord(ev_mid, st));
+  if (mk) mk->mark(st, 2);
   const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
                         (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
@@ -225,42 +242,62 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
 }
 
 void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
-               cudaEvent_t ev_mid = nullptr) {
-  if (t.kind == 1) return launch_dmma(t, arena, ptrs_d, tab_d, st, ev_mid);
-  auto pack = [&](const PackDesc& d, int64_t off, int) {
+               Marks* mk = nullptr) {
+  if (t.kind == 1) return launch_dmma(t, arena, ptrs_d, tab_d, st, mk);
+  auto pack = [&](const PackDesc& d, int64_t off, int64_t base) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
-    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(ptrs_d, d, tab_d,
-                                                              reinterpret_cast<__nv_bfloat16*>(arena + off));
+    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
+        ptrs_d, d, tab_d, reinterpret_cast<__nv_bfloat16*>(arena + off), base);
     g_launches++;
   };
-  pack(t.px, t.x_off, t.m_bits);
-  pack(t.py, t.y_off, t.n_bits);
-  if (ev_mid) CK(cudaEventRecord(ev_mid, st));
   const int64_t tiles = (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN) * (((int64_t(1) << t.m_bits) + 127) / 128);
   dim3 grid((unsigned)tiles, 1, (unsigned)((1u << t.nb_bits) * t.S));
   float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
-  if (t.BN == 128) {
-    ensure_gemm_attr<128>();
-    tnd::tc::cgemm_bf16x6_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
-        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, KC_PER_SPLIT, partial);
-  } else {
-    ensure_gemm_attr<64>();
-    tnd::tc::cgemm_bf16x6_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
-        t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, 1 << t.nb_bits, KC_PER_SPLIT, partial);
-  }
-  g_launches++;
-  if (t.S > 1) {
-    const int64_t n = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
-    tnd::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, t.S, n, ptrs_d, t.c_node);
+  for (int s = 0; s < t.n_slabs; ++s) {
+    if (mk) mk->mark(st, 1);
+    pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
+    pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
+    if (mk) mk->mark(st, 2);
+    const int acc = s > 0;
+    if (t.BN == 128) {
+      ensure_gemm_attr<128>();
+      tnd::tc::cgemm_bf16x6_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
+          t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+          partial, acc);
+    } else {
+      ensure_gemm_attr<64>();
+      tnd::tc::cgemm_bf16x6_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
+          t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+          partial, acc);
+    }
     g_launches++;
+    if (t.S > 1) {
+      if (mk) mk->mark(st, 3);
+      const int64_t n = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+      const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+      tnd::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, t.S, n, ptrs_d, t.c_node, acc);
+      g_launches++;
+    }
   }
   CK(cudaGetLastError());
 }
 
+// entries of one packed K-slab operand: 2^30 (12 GB for complex64); TN_PACK_CAP_LOG2
+// overrides it (tests force K-slabs on small shapes)
+int pack_cap_log2() {
+  static int v = [] {
+    const char* e = std::getenv("TN_PACK_CAP_LOG2");
+    return e ? std::atoi(e) : 30;
+  }();
+  return v;
+}
+
 void finish_tc_shape(TcStep& t) {
   t.BN = (t.n_bits >= 7) ? 128 : 64;
-  const int64_t nk_all = ((int64_t(1) << t.k_bits) + tnd::tc::BK - 1) / tnd::tc::BK;
+  const int over = std::max(t.nb_bits + t.m_bits, t.nb_bits + t.n_bits) + t.k_bits - pack_cap_log2();
+  t.k_lo = std::max(std::min(t.k_bits, 5), t.k_bits - std::max(0, over));
+  t.n_slabs = 1 << (t.k_bits - t.k_lo);
+  const int64_t nk_all = ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK;
   t.S = (int)((nk_all + KC_PER_SPLIT - 1) / KC_PER_SPLIT);
 }
 int64_t tc_partial_bytes(const TcStep& t) {
@@ -293,14 +330,19 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
 
 // Pack descriptor: bit permutation from the operand's stored layout to [b][rows][k]
 // (destination planes [b][6][rows][k]); see pack_bf16x3_kernel.
+// k_lo < k bits: only the lowest k_lo bits of the k group are packed (a K-slab); the
+// source offsets of the remaining high k bits, one per slab, are appended to `slabs`.
 PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
                    const std::vector<int>& rows, const std::vector<int>& kg, const std::vector<int>& l2,
-                   int planes = 6) {
+                   int planes = 6, int k_lo = -1, std::vector<int64_t>* slabs = nullptr) {
   PackDesc d{};
   d.src = src_node;
   d.nb_bits = sum_bits(batch, l2);
   d.r_bits = sum_bits(rows, l2);
-  d.k_bits = sum_bits(kg, l2);
+  const int k_all = sum_bits(kg, l2);
+  if (k_lo < 0 || k_lo > k_all) k_lo = k_all;
+  d.k_bits = k_lo;
+  const int D_all = d.nb_bits + d.r_bits + k_all;
   const int D = d.nb_bits + d.r_bits + d.k_bits, RK = d.r_bits + d.k_bits;
   d.plane = int64_t(1) << RK;
   // source bit of every destination bit
@@ -312,13 +354,24 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   std::vector<int> order = batch;
   order.insert(order.end(), rows.begin(), rows.end());
   order.insert(order.end(), kg.begin(), kg.end());
-  std::vector<int> pi(D);
+  std::vector<int> pi_all(D_all), pi(D);
   {
     int sh = 0;
     for (int k = (int)order.size() - 1; k >= 0; --k) {
       int i = order[k];
-      for (int u = 0; u < l2[i]; ++u) pi[sh + u] = src_shift.at(i) + u;
+      for (int u = 0; u < l2[i]; ++u) pi_all[sh + u] = src_shift.at(i) + u;
       sh += l2[i];
+    }
+  }
+  // destination bits: k bits [0, k_lo) stay, [k_lo, k_all) are fixed per slab, the
+  // rest shift down by k_all - k_lo
+  for (int j = 0; j < D; ++j) pi[j] = j < k_lo ? pi_all[j] : pi_all[j + (k_all - k_lo)];
+  if (slabs) {
+    slabs->clear();
+    for (int64_t s = 0; s < (int64_t(1) << (k_all - k_lo)); ++s) {
+      int64_t o = 0;
+      for (int u = 0; u < k_all - k_lo; ++u) if ((s >> u) & 1) o += int64_t(1) << pi_all[k_lo + u];
+      slabs->push_back(o);
     }
   }
   auto dst_contrib = [&](int dbit) -> int64_t {
@@ -373,10 +426,10 @@ bool want_tc(int dtype, int nb, int m, int n, int k) {
 }
 void finish_tc_kind(TcStep& t, int dtype) {
   t.kind = dtype == TN_C128 ? 1 : 0;
-  if (t.kind == 1) { t.S = 1; t.BN = tnd::zg::BN; }
+  if (t.kind == 1) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; }
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
-  return (t.kind == 1 ? int64_t(16) : int64_t(12)) << (t.nb_bits + rows_bits + t.k_bits);
+  return (t.kind == 1 ? int64_t(16) : int64_t(12)) << (t.nb_bits + rows_bits + t.k_lo);
 }
 
 // first-fit offsets for (size, [lo, hi]) items
@@ -462,7 +515,7 @@ struct tn_plan_s {
         k += 1;
       } else {
         launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
-        k += tcs[L.second].S > 1 ? 4 : 3;
+        k += tcs[L.second].kind ? 3 : tcs[L.second].n_slabs * (tcs[L.second].S > 1 ? 4 : 3);
       }
     }
     if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
@@ -610,8 +663,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       finish_tc_shape(t);
       t.c_node = c;
       finish_tc_kind(t, P.dtype);
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 6);
-      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 6);
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_y);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -702,29 +755,35 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
 
   for (size_t k = 0; k < ord.steps.size(); ++k) P.step_table[6 * k + 5] = step_pos[k];
   // ---- arena: intermediates + pack buffers, first fit over live intervals ----
+  // Every launch position L has two phases: 2L (tensor-core packs read the raw operands)
+  // and 2L+1 (GEMM / small wave).  A tensor-core step's raw operands die after its pack
+  // phase, its pack buffers live through both phases, its output is born at 2L+1.
   std::vector<int64_t> sizes;
   std::vector<std::pair<int, int>> ivs;
-  std::vector<int> owner;  // >=0: node id; -1 - 2*tc: pack X; -2 - 2*tc: pack Y
-  const int last = (int)P.launches.size();
+  std::vector<int> owner;  // >=0: node id; -1 - 2*tc: pack X; -2 - 2*tc: pack Y; <= -1000000: partials
+  const int last = 2 * (int)P.launches.size() + 2;
   for (size_t k = 0; k < ord.steps.size(); ++k) {
     int c = n + (int)k;
-    int hi = parent[c] >= 0 ? step_pos[parent[c]] : last;
+    int born = 2 * step_pos[k] + 1;
+    int hi = last;
+    if (parent[c] >= 0) hi = 2 * step_pos[parent[c]] + (kind[parent[c]] ? 0 : 1);
     sizes.push_back((int64_t(1) << L[c].bits) * P.esz);
-    ivs.push_back({step_pos[k], hi});
+    ivs.push_back({born, hi});
     owner.push_back(c);
   }
   for (size_t k = 0; k < ord.steps.size(); ++k) {
     if (!kind[k]) continue;
     const auto& t = P.tcs[big_index[k]];
+    const int p0 = 2 * step_pos[k];
     sizes.push_back(pack_bytes(t, t.m_bits));
-    ivs.push_back({step_pos[k], step_pos[k]});
+    ivs.push_back({p0, p0 + 1});
     owner.push_back(-1 - 2 * big_index[k]);
     sizes.push_back(pack_bytes(t, t.n_bits));
-    ivs.push_back({step_pos[k], step_pos[k]});
+    ivs.push_back({p0, p0 + 1});
     owner.push_back(-2 - 2 * big_index[k]);
     if (t.S > 1) {
       sizes.push_back(tc_partial_bytes(t));
-      ivs.push_back({step_pos[k], step_pos[k]});
+      ivs.push_back({p0 + 1, p0 + 1});
       owner.push_back(-1000000 - big_index[k]);
     }
   }
@@ -749,8 +808,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   }
   for (auto& t : P.tcs) {
     if (t.kind == 1) continue;
-    t.ta = make_plane_map(P.arena + t.x_off, t.k_bits, t.m_bits, t.nb_bits, 128, 6);
-    t.tb = make_plane_map(P.arena + t.y_off, t.k_bits, t.n_bits, t.nb_bits, t.BN, 6);
+    t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 6);
+    t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.BN, 6);
   }
 
   // ---- uploads ----
@@ -795,66 +854,52 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
 
 void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_profile& pr) {
   std::memset(&pr, 0, sizeof(pr));
-  const size_t nl = P.launches.size();
-  std::vector<cudaEvent_t> ev(2 * nl + 4);
-  std::vector<cudaEvent_t> mid(nl, nullptr);
-  for (auto& e : ev) CK(cudaEventCreate(&e));
-  for (size_t j = 0; j < nl; ++j)
-    if (P.launches[j].first == 1) CK(cudaEventCreate(&mid[j]));
   for (int64_t s = s0; s < s1; ++s) {
-    CK(cudaEventRecord(ev[0], st));
+    Marks mk;
+    mk.mark(st, 4);
     tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
         P.ptrs_d, P.leaf_base_d, P.var_begin_d, P.var_kind_d, P.var_stride_d, P.n_leaves, P.bits_d, P.slice_d,
         P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
     g_launches++;
-    CK(cudaEventRecord(ev[1], st));
-    for (size_t j = 0; j < nl; ++j) {
-      const auto& L = P.launches[j];
-      CK(cudaEventRecord(ev[2 + 2 * j], st));
+    pr.n_other++;
+    for (const auto& L : P.launches) {
       if (L.first == 0) {
+        mk.mark(st, 0);
         if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
         else launch_wave<double>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
-      } else {
-        launch_tc(P.tcs[L.second], P.arena, P.ptrs_d, P.tab_d, st, mid[j]);
-      }
-      CK(cudaEventRecord(ev[3 + 2 * j], st));
-    }
-    CK(cudaEventRecord(ev[2 + 2 * nl], st));
-    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
-    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
-    g_launches++;
-    CK(cudaEventRecord(ev[3 + 2 * nl], st));
-    CK(cudaEventSynchronize(ev[3 + 2 * nl]));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-    pr.ms_other += ms;
-    CK(cudaEventElapsedTime(&ms, ev[2 + 2 * nl], ev[3 + 2 * nl]));
-    pr.ms_other += ms;
-    pr.n_other += 2;
-    for (size_t j = 0; j < nl; ++j) {
-      const auto& L = P.launches[j];
-      if (L.first == 0) {
-        CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], ev[3 + 2 * j]));
-        pr.ms_small += ms;
-        pr.n_small += 1;
+        pr.n_small++;
         pr.flops_small += P.waves[L.second].flops;
         pr.bytes_small += P.waves[L.second].bytes;
       } else {
         const auto& t = P.tcs[L.second];
-        CK(cudaEventElapsedTime(&ms, ev[2 + 2 * j], mid[j]));
-        pr.ms_pack += ms;
-        CK(cudaEventElapsedTime(&ms, mid[j], ev[3 + 2 * j]));
-        pr.ms_gemm += ms;
-        pr.n_pack += 2;
-        pr.n_gemm += 1;
+        launch_tc(t, P.arena, P.ptrs_d, P.tab_d, st, &mk);
+        pr.n_gemm += t.kind ? 1 : t.n_slabs;
+        pr.n_pack += 2 * (t.kind ? 1 : t.n_slabs);
         pr.flops_gemm += t.flops;
-        pr.bytes_pack += 20.0 * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +   // read 8 B, write 12 B
-                                 std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits));
+        pr.bytes_pack += (t.kind ? 24.0 : 20.0) * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
+                                                   std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits));
       }
     }
+    mk.mark(st, 4);
+    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
+    g_launches++;
+    pr.n_other++;
+    mk.mark(st, -1);
+    CK(cudaEventSynchronize(mk.v.back().first));
+    for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, mk.v[j].first, mk.v[j + 1].first));
+      switch (mk.v[j].second) {
+        case 0: pr.ms_small += ms; break;
+        case 1: pr.ms_pack += ms; break;
+        case 2: pr.ms_gemm += ms; break;
+        case 3: pr.ms_other += ms; break;     // split-K reduction
+        default: pr.ms_other += ms; break;
+      }
+    }
+    for (auto& e : mk.v) cudaEventDestroy(e.first);
   }
-  for (auto& e : ev) cudaEventDestroy(e);
-  for (auto& e : mid) if (e) cudaEventDestroy(e);
 }
 
 void run_slices(tn_plan_s& P, const uint8_t* bits, bool bits_on_device, int64_t s0, int64_t s1, cudaStream_t st) {
@@ -1179,8 +1224,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       finish_tc_shape(t);
       finish_tc_kind(t, dtype);
       t.c_node = 2;
-      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 6);
-      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 6);
+      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_y);
       size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
@@ -1190,8 +1235,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
       if (t.kind == 0) {
-        t.ta = make_plane_map(scratch + t.x_off, kk, mx, nb, 128, 6);
-        t.tb = make_plane_map(scratch + t.y_off, kk, my, nb, t.BN, 6);
+        t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 6);
+        t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.BN, 6);
       }
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies

@@ -12,6 +12,7 @@ Tolerances (DESIGN.md "Tolerances"):
     RMS amplitude 2^{-n/2} as the scale for amplitudes near zero)
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -138,6 +139,28 @@ def test_pair_complex128_dmma_path(case):
     ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
     got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
     assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
+
+
+def test_pair_tensor_core_k_slabs(monkeypatch):
+    """K-slab packing (bounded pack buffers): forced by lowering the pack cap in a child
+    process (the cap is read once per process)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        sys.path.insert(0, 'tests')
+        import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
+        for case in [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2)]:
+            nb, m, n, k, ps = case
+            ia, ib, ic, dims = T._gemm_case(nb, m, n, k, ps)
+            got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=31)
+            err = np.abs(got - ref)
+            assert np.all(err <= T.c64_tol(2 ** k) * bound + 1e-30), (case, (err / bound).max())
+        print('ok')
+    """)
+    env = dict(os.environ, TN_PACK_CAP_LOG2="13")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_pair_tc_matches_small_path():
