@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "contraction FLOP/s"
 CONFIG_IDX = 1
-SLICE_LOGS = (32, 31)    # largest tensor of a slice: 2^32 complex64 = 32 GB (arena ~160 GB), else 2^31
+SLICE_LOGS = (34, 33, 32, 31)   # largest tensor of a slice: 2^34 complex64 = 128 GB-class plan (arena ~170 GB), else smaller
 ORDER_SEED = 0
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # split-precision complex64: one complex MAC = 4 real products x 6 bf16 piece products
@@ -135,7 +135,7 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=SLICE_LOGS[0]):
         uni = (set(Ai) | set(Bi)) - set(fixed)
         m = sum(int(math.log2(net.dims[i])) for i in uni)
         nodes.pop(a), nodes.pop(b)
-        if m > 29:        # bounded sample: steps too large for the CPU budget are skipped
+        if m > 33:        # bounded sample: steps too large for the CPU budget are skipped
             skipped += 1
             continue
         kk = [i for i in kept[k] if i not in fixed]
@@ -147,7 +147,7 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=SLICE_LOGS[0]):
     el = time.perf_counter() - t0
     return {"value": flops / el, "unit": "FLOP/s", "cores": int(cores), "kind": "oracle",
             "sample": f"oracle (numpy complex128) on slice 0 of bitstring 0: {done} of the {len(steps)} pairwise "
-                      f"steps of the separator tree in order, skipping {skipped} steps with M > 2^29 or depending on "
+                      f"steps of the separator tree in order, skipping {skipped} steps with M > 2^33 or depending on "
                       f"one ({flops:.3g} flops, {el:.1f} s)"}
 
 
@@ -263,7 +263,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": "configs[1]: 8x8 lattice, depth 16, Haar U(2) + CZ brickwork; complex64 "
-                               "(bf16x6 split on tcgen05); separator order seed 0; slicing to 2^31-entry tensors",
+                               f"(bf16x6 split on tcgen05); separator order seed 0; slicing to 2^{slice_log2}-entry tensors",
                    "step": f"one slice (of {n_slices}) of one amplitude; rank r takes bitstrings r::N of 1024",
                    "flops_per_step": flops_slice, "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice,
                    "n_slices_per_amplitude": n_slices, "l2": "working set (GB intermediates) >> 126 MB L2, no flush",
@@ -296,7 +296,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
