@@ -3,7 +3,7 @@
 amplitudes/s on B200, % of tensor-pipe peak).
 
 Workload (N=1): configs[1] -- 8x8 qubit lattice, depth 16, Haar U(2) + CZ brickwork,
-complex64 on split-precision (bf16x6) tensor cores, separator order (SM Algorithm 1)
+complex64 on block-scaled fp16x2 split-precision tensor cores, separator order (SM Algorithm 1)
 sliced so every tensor fits HBM.  Its amplitudes are partitioned by bitstring across
 ranks (weak scaling): rank r contracts bitstrings r, r+N, ... of the seeded batch of
 1024.  One STEP = one slice of one amplitude (the whole separator tree over one
@@ -34,8 +34,9 @@ CONFIG_IDX = 1
 SLICE_LOGS = (34, 33, 32, 31)   # largest tensor of a slice: 2^34 complex64 = 128 GB-class plan (arena ~170 GB), else smaller
 ORDER_SEED = 0
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# split-precision complex64: one complex MAC = 4 real products x 6 bf16 piece products
-BF16_FLOPS_PER_USEFUL = 48.0 / 8.0
+# split-precision complex64: one complex MAC (8 useful flops) = 4 real products x 3 fp16
+# piece products (hi.hi, hi.lo, lo.hi) = 24 fp16 tensor flops; fp16 dense rate = bf16 rate
+F16_FLOPS_PER_USEFUL = 24.0 / 8.0
 
 
 def load_peaks():
@@ -256,14 +257,14 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return 0
     peaks, peak_src = load_peaks()
-    peak_tc = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / BF16_FLOPS_PER_USEFUL
+    peak_tc = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / F16_FLOPS_PER_USEFUL
     gemm_tfs = prof["flops_gemm"] / (prof["ms_gemm"] / 1e3) / 1e12 if prof.get("ms_gemm") else 0.0
     line = {
         "metric": METRIC, "value": value, "unit": "FLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": "configs[1]: 8x8 lattice, depth 16, Haar U(2) + CZ brickwork; complex64 "
-                               f"(bf16x6 split on tcgen05); separator order seed 0; slicing to 2^{slice_log2}-entry tensors",
+                               f"(block-scaled fp16x2 split on tcgen05); separator order seed 0; slicing to 2^{slice_log2}-entry tensors",
                    "step": f"one slice (of {n_slices}) of one amplitude; rank r takes bitstrings r::N of 1024",
                    "flops_per_step": flops_slice, "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice,
                    "n_slices_per_amplitude": n_slices, "l2": "working set (GB intermediates) >> 126 MB L2, no flush",
@@ -271,9 +272,9 @@ def run_ours(args):
         "amplitudes_per_s": amps_per_s,
         "roofline": {"bound": "tensor", "achieved": gemm_tfs, "peak": peak_tc, "unit": "TFLOP/s",
                      "frac": gemm_tfs / peak_tc if peak_tc else None, "traffic": None,
-                     "kernel": "cgemm_bf16x6_kernel (tcgen05)",
-                     "peak_note": f"{peak_src} bf16 sustained {peaks.get('bf16_tflops_sustained')} TF/s x 8/48 "
-                                  "(useful complex flops per bf16 flop of the bf16x6 scheme)",
+                     "kernel": "cgemm_f16x2s_kernel (tcgen05)",
+                     "peak_note": f"{peak_src} bf16 sustained {peaks.get('bf16_tflops_sustained')} TF/s (= fp16 dense rate) "
+                                  "x 8/24 (useful complex flops per fp16 tensor flop of the fp16x2 scheme)",
                      "share_of_step": prof["ms_gemm"] / ms if ms else None},
         "kernel_ms": {k: prof[k] for k in ("ms_gemm", "ms_pack", "ms_small", "ms_other")},
         "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(c.n),

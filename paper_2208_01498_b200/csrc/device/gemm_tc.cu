@@ -5,19 +5,24 @@
 //   C[b][m][n] = sum_k A[b][m][k] * B[b][k][n].
 //
 // Precision scheme: every fp32 component x of A and B
-// is split into three bf16 pieces x = x0 + x1 + x2 (each the bf16 rounding of the
-// remainder); the six products x_i y_j with i + j <= 2 are accumulated in fp32 on
-// tcgen05 (kind::f16, bf16 inputs, fp32 accumulators in TMEM).  Complex arithmetic
-// is planar: Cr += Ar.Br + (-Ai).Bi, Ci += Ar.Bi + Ai.Br, the minus sign taken by
-// the instruction descriptor's negate-A bit, so no operand is ever expanded.
+// is scaled by a power of two per (row, 32-element K chunk) so the chunk maximum lies
+// just below 2^14, then split into two fp16 pieces x = x0 + x1 (x0 = fp16(x),
+// x1 = fp16(x - x0)): 22 significand bits, the representation error is
+// <= 2^-24 |x| + 2^-39 max|chunk|.  The three products x0 y0, x0 y1, x1 y0 are
+// accumulated in fp32 on tcgen05 (kind::f16, fp16 inputs, fp32 accumulators in TMEM);
+// the dropped x1 y1 is <= 2^-24 |x y|.  That is fp32-level accuracy at 3 MMAs per real
+// product (bf16x3 splitting needs 6).  Complex arithmetic is planar:
+// Cr += Ar.Br + (-Ai).Bi, Ci += Ar.Bi + Ai.Br, the minus sign taken by the instruction
+// descriptor's negate-A bit, so no operand is ever expanded.
 //
-// Pipeline: pack kernel (fused permutation to matricised [b][rows][k] form + bf16x3
-// split, one HBM pass) -> TMA (SWIZZLE_64B, 3-D maps over planes) into a 2/3-stage
-// mbarrier ring -> one elected thread issues tcgen05.mma into ping-pong TMEM buffers
-// -> epilogue warps promote each stage into fp32 registers (tcgen05.ld) and finally
-// write interleaved complex64 C (or a split-K partial).
+// Pipeline: pack kernel (fused permutation to matricised [b][rows][k] form + scale +
+// fp16x2 split, one HBM pass) -> TMA (SWIZZLE_64B, 3-D maps over the 4 planes) and bulk
+// copies of the chunk scales into mbarrier rings -> one elected thread issues
+// tcgen05.mma into ping-pong TMEM buffers -> epilogue warps promote each stage, scaled,
+// into fp32 registers (tcgen05.ld) and finally write interleaved complex64 C (or a
+// split-K partial).
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -42,7 +47,7 @@ struct PackDesc {
   int64_t e_q;                      // tab[e_q + e]: compact destination index of e
   GroupMap tile_src, tile_dst;      // tile id -> source / destination element offset
   GroupMap q_hi;                    // (q >> ld) -> destination offset
-  int64_t plane;                    // rows * K: elements per bf16 plane
+  int64_t plane;                    // rows * K: elements per plane
 };
 
 constexpr int PACK_MAX_T = 11;
@@ -54,30 +59,38 @@ constexpr int PACK_PER_THREAD = (1 << PACK_MAX_T) / PACK_THREADS;   // 8
 // for the 16-byte loads of phase 2.
 __device__ __forceinline__ int pack_slot(int q) { return q ^ ((((q >> 4) ^ (q >> 7) ^ (q >> 10)) & 7) << 1); }
 
-// split 2 floats into 3 bf16x2 pieces (each the bf16 rounding of the remainder)
-__device__ __forceinline__ void split3x2(float a, float b, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+// Block scaling: every chunk of SCALE_CHUNK consecutive K
+// elements of one row (re and im together) gets a power-of-two scale 2^(e-14), e the
+// exponent with max|x| < 2^e, so the scaled chunk lies in (-2^14, 2^14): the top of the
+// fp16 range, which keeps the second piece of elements far below the chunk maximum out
+// of the fp16 subnormals (absolute floor 2^-25 * 2^-14 of the chunk maximum).
+constexpr int SCALE_CHUNK = 32;
+
+// split two scaled floats into two fp16x2 pieces: hi = fp16(x), lo = fp16(x - hi)
+__device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_t& p1) {
+  __half2 h = __floats2half2_rn(a, b);
   p0 = *reinterpret_cast<uint32_t*>(&h);
-  float ra = a - __low2float(h), rb = b - __high2float(h);
-  h = __floats2bfloat162_rn(ra, rb);
+  const float2 f = __half22float2(h);
+  h = __floats2half2_rn(a - f.x, b - f.y);
   p1 = *reinterpret_cast<uint32_t*>(&h);
-  ra = ra - __low2float(h);
-  rb = rb - __high2float(h);
-  h = __floats2bfloat162_rn(ra, rb);
-  p2 = *reinterpret_cast<uint32_t*>(&h);
 }
 
-// out planes, layout [b][plane][r][k] bf16, plane = 2 * piece + {0: re, 1: im}.
-// Tiles have 2^t_bits elements, 3 <= t_bits <= PACK_MAX_T (11 unless the operand is smaller).
-__global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+// out planes, layout [b][4][r][k] fp16, plane = 2 * piece + {0: re, 1: im}; scales
+// [b][K / 32][r] fp32 (one per row and 32-element K chunk; one per row if K < 32).
+// Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
+// inside the tile, so every K chunk is held by 2 or 4 adjacent threads of one warp.
+__global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
-                                                                   __nv_bfloat16* __restrict__ out, int64_t src_base) {
+                                                                   __half* __restrict__ out, float* __restrict__ scales,
+                                                                   int64_t src_base) {
   __shared__ __align__(16) float2 s[1 << PACK_MAX_T];
   const float2* __restrict__ src = reinterpret_cast<const float2*>(ptrs[d.src]) + src_base;
   const int64_t n_tiles = int64_t(1) << d.tile_bits;
   const int64_t lmask = (int64_t(1) << d.ld) - 1;
   const int T = 1 << d.t_bits;
-  // tile-independent local offsets, cached in registers
+  const int RK = d.r_bits + d.k_bits;
+  const int chunk_log2 = min(d.k_bits, 5);             // log2 elements per scale
+  const int nch_log2 = max(d.k_bits - 5, 0);           // log2 chunks per row
   int64_t so[PACK_PER_THREAD];
   int sl[PACK_PER_THREAD];
 #pragma unroll
@@ -87,7 +100,7 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* c
     sl[i] = e < T ? pack_slot((int)__ldg(tab + d.e_q + e)) : 0;
   }
   const int q0 = threadIdx.x * 8;                       // this thread's 8 destination elements
-  const bool writer = q0 < T;
+  const bool writer = q0 < T;                           // uniform per warp (T >= 256)
   const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t sb = gmap(tab, d.tile_src, tile);
@@ -105,19 +118,32 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* c
     for (int j = 0; j < 4; ++j) w[j] = writer ? *reinterpret_cast<const float4*>(&s[pack_slot(q0 + 2 * j)]) : float4{};
     __syncthreads();
     if (!writer) continue;
-    // w[j] = (re_{2j}, im_{2j}, re_{2j+1}, im_{2j+1}); slots of a pair are adjacent
-    uint4 o[6];
+    // chunk maximum over |re|, |im| (chunk = 2^chunk_log2 elements = 2^(chunk_log2-3) threads)
+    float m = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m = fmaxf(m, fmaxf(fmaxf(fabsf(w[j].x), fabsf(w[j].y)), fmaxf(fabsf(w[j].z), fabsf(w[j].w))));
+    for (int o = 1; o < (1 << (chunk_log2 - 3)); o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    frexpf(m, &e);                                       // m < 2^e (e = 0 for m = 0)
+    // scale up by 2^(14-e), exact; two factors when 14-e exceeds the fp32 exponent range
+    const float upc = ldexpf(1.f, min(14 - e, 127));
+    const float up2 = ldexpf(1.f, max(14 - e - 127, 0));
+    uint4 o[4];
     uint32_t* op = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t r0, r1, r2, i0, i1, i2;
-      split3x2(w[j].x, w[j].z, r0, r1, r2);
-      split3x2(w[j].y, w[j].w, i0, i1, i2);
-      op[0 * 4 + j] = r0; op[1 * 4 + j] = i0; op[2 * 4 + j] = r1;
-      op[3 * 4 + j] = i1; op[4 * 4 + j] = r2; op[5 * 4 + j] = i2;
+      uint32_t r0, r1, i0, i1;
+      split2x2(w[j].x * upc * up2, w[j].z * upc * up2, r0, r1);
+      split2x2(w[j].y * upc * up2, w[j].w * upc * up2, i0, i1);
+      op[0 * 4 + j] = r0; op[1 * 4 + j] = i0; op[2 * 4 + j] = r1; op[3 * 4 + j] = i1;
     }
 #pragma unroll
-    for (int p = 0; p < 6; ++p) *reinterpret_cast<uint4*>(out + db + p * d.plane) = o[p];
+    for (int p = 0; p < 4; ++p) *reinterpret_cast<uint4*>(out + db + p * d.plane) = o[p];
+    if ((threadIdx.x & ((1 << (chunk_log2 - 3)) - 1)) == 0) {
+      const int64_t bb = db >> (RK + 2), rk = db & (d.plane - 1);
+      const int64_t r = rk >> d.k_bits, kc = (rk & ((int64_t(1) << d.k_bits) - 1)) >> 5;
+      scales[(((bb << nch_log2) + kc) << d.r_bits) + r] = ldexpf(1.f, e - 14);
+    }
   }
 }
 
@@ -125,23 +151,24 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_bf16x3_kernel(const void* c
 namespace tc {
 
 constexpr int BM = 128;    // rows per tile (TMEM lanes)
-constexpr int BK = 32;     // bf16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
-constexpr int PROMO = 1;   // smem stages accumulated per TMEM buffer before promotion
+constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B) = one scale chunk
 constexpr int GROUP_M = 8; // CTA rasterization: 8 M-tiles share each B panel in flight
 
 template <int BN>
 struct Cfg {
-  static constexpr int A_PLANE = BM * BK * 2;              // one bf16 plane tile
+  static constexpr int A_PLANE = BM * BK * 2;              // one fp16 plane tile
   static constexpr int B_PLANE = BN * BK * 2;
-  static constexpr int A_BYTES = 6 * A_PLANE;              // 3 pieces x (re, im)
-  static constexpr int B_BYTES = 6 * B_PLANE;
+  static constexpr int A_BYTES = 4 * A_PLANE;              // 2 pieces x (re, im)
+  static constexpr int B_BYTES = 4 * B_PLANE;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (3 * STAGE + 2048 <= 227 * 1024) ? 3 : 2;
+  static constexpr int SLOTS = 8;                          // scale ring (epilogue lags the MMA)
+  static constexpr int SC_BYTES = (BM + BN) * 4;           // A and B chunk scales of one stage
+  static constexpr int STAGES = (4 * STAGE + SLOTS * SC_BYTES + 2048 <= 227 * 1024) ? 4 : 3;
   static constexpr int ACC_COLS = 2 * BN;                  // [re | im] of one accumulator buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS;           // ping-pong buffers
   static constexpr int EPI_WARPS = 4 * (BN / 64);          // each owns 32 rows x 64 columns
   static constexpr int THREADS = 32 * (EPI_WARPS + 2);     // + TMA warp + MMA warp
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + SLOTS * SC_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -173,6 +200,13 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// plain bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // K-major operand tile with 64-byte rows, SWIZZLE_64B: 8-row atoms of 512 B.
 __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem) {
   const uint64_t addr = smem_u32(smem);
@@ -184,7 +218,7 @@ __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem) {
   d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
   return d;
 }
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -195,6 +229,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -203,27 +242,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-// Precision: the tensor core's fp32 accumulation
-// truncates, so an accumulator updated T times drifts by ~T/4 ulp toward zero.  Every
-// 32 elements of K (one smem stage) are therefore accumulated in a fresh TMEM buffer
-// (24 MMA updates per element) and promoted by the epilogue warps into fp32 registers
-// with round-to-nearest adds; two TMEM buffers ping-pong so promotion overlaps the
-// next MMAs.  (A variant with one m128 x n256 MMA over stacked [Br; Bi] / [-Bi; Br]
-// tiles cut shared-memory operand traffic by 25% but needed 32-byte TMA rows and ran
-// slower; the kernel is at the power-capped bf16 throughput anyway -- DESIGN.md.)
+// Complex GEMM C[b][m][n] (+)= sum_k A[b][m][k] B[b][n][k] on block-scaled fp16x2
+// operands.  Per 32-wide K stage the MMA warp issues
+// 2 (k16) x 3 piece pairs (hi.hi, hi.lo, lo.hi) x 4 real products = 24 MMAs into a fresh
+// TMEM buffer; the epilogue warps promote it into fp32 registers, multiplying by the
+// stage's chunk scales sA[row] * sB[col] (round-to-nearest; tcgen05 fp32 accumulation
+// truncates, so no accumulator sees more than 12 updates).  Two TMEM buffers ping-pong.
 template <int BN>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
-    cgemm_bf16x6_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    cgemm_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const float* __restrict__ scA, const float* __restrict__ scB,
                         void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
                         int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate) {
   using CF = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE);
+  float* sc = reinterpret_cast<float*>(smem + CF::STAGES * CF::STAGE);   // [SLOTS][BM + BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE + CF::SLOTS * CF::SC_BYTES);
   uint64_t* empty = full + CF::STAGES;
   uint64_t* tfull = empty + CF::STAGES;     // [2] MMA -> epilogue: buffer holds a finished stage
   uint64_t* tempty = tfull + 2;             // [2] epilogue -> MMA: buffer promoted
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;             // [SLOTS] scales landed
+  uint64_t* sempty = sfull + CF::SLOTS;     // [SLOTS] scales consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + CF::SLOTS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TMA_WARP = CF::EPI_WARPS, MMA_WARP = CF::EPI_WARPS + 1;
@@ -240,11 +281,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   const int nk_all = (K + BK - 1) / BK;
   const int kc0 = split * kc_per_split;
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
-  const int n_promo = (nk + PROMO - 1) / PROMO;
 
   if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CF::EPI_WARPS); }
+    for (int s = 0; s < CF::SLOTS; ++s) { mbar_init(&sfull[s], 1); mbar_init(&sempty[s], CF::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -261,31 +302,36 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 
   if (warp == TMA_WARP) {
     if (lane == 0) {
+      const float* sa = scA + ((int64_t)b * nk_all) * M + m_blk * BM;
+      const float* sb = scB + ((int64_t)b * nk_all) * N + n_blk * BN;
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % CF::STAGES;
         const uint32_t ph = (kc / CF::STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], CF::STAGE);
         uint8_t* st = smem + s * CF::STAGE;
-        tma_load_3d(&tmA, st, &full[s], (kc0 + kc) * BK, m_blk * BM, b * 6);               // 6 planes
-        tma_load_3d(&tmB, st + CF::A_BYTES, &full[s], (kc0 + kc) * BK, n_blk * BN, b * 6); // 6 planes
+        tma_load_3d(&tmA, st, &full[s], (kc0 + kc) * BK, m_blk * BM, b * 4);               // 4 planes
+        tma_load_3d(&tmB, st + CF::A_BYTES, &full[s], (kc0 + kc) * BK, n_blk * BN, b * 4); // 4 planes
+        const int slot = kc % CF::SLOTS;
+        mbar_wait(&sempty[slot], ((kc / CF::SLOTS) & 1) ^ 1);
+        mbar_expect_tx(&sfull[slot], CF::SC_BYTES);
+        float* d = sc + slot * (BM + BN);
+        bulk_load(d, sa + (int64_t)(kc0 + kc) * M, BM * 4, &sfull[slot]);
+        bulk_load(d + BM, sb + (int64_t)(kc0 + kc) * N, BN * 4, &sfull[slot]);
       }
     }
   } else if (warp == MMA_WARP) {
     if (lane == 0) {
-      // idesc: F32 accumulate, BF16 A/B, K-major both, N = BN, M = 128
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      // idesc: F32 accumulate, F16 A/B, K-major both, N = BN, M = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       const uint32_t idesc_negA = idesc | (1u << 13);
-      const int PA[6] = {0, 0, 1, 0, 1, 2};
-      const int PB[6] = {0, 1, 0, 2, 1, 0};
+      const int PA[3] = {0, 0, 1};
+      const int PB[3] = {0, 1, 0};
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % CF::STAGES;
         const uint32_t ph = (kc / CF::STAGES) & 1;
-        const int pi = kc / PROMO;
-        const int buf = pi & 1;
-        const bool first = (kc % PROMO) == 0;
-        const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
-        if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // epilogue drained this buffer
+        const int buf = kc & 1;
+        mbar_wait(&tempty[buf], ((kc >> 1) & 1) ^ 1);   // epilogue drained this buffer
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
@@ -293,51 +339,57 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < BK / 16; ++ks) {
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
+          for (int q = 0; q < 3; ++q) {
             const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
             const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
             const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
             const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;   // fresh accumulator per promotion
-            mma_bf16(t_re, a_re, b_re, idesc, acc);
-            mma_bf16(t_re, a_im, b_im, idesc_negA, 1u);
-            mma_bf16(t_im, a_re, b_im, idesc, acc);
-            mma_bf16(t_im, a_im, b_re, idesc, 1u);
+            const uint32_t acc = ((ks | q) == 0) ? 0u : 1u;   // fresh accumulator per stage
+            mma_f16(t_re, a_re, b_re, idesc, acc);
+            mma_f16(t_re, a_im, b_im, idesc_negA, 1u);
+            mma_f16(t_im, a_re, b_im, idesc, acc);
+            mma_f16(t_im, a_im, b_re, idesc, 1u);
           }
         }
-        mma_commit(&empty[s]);                 // smem stage free once these MMAs have read it
-        if (last) mma_commit(&tfull[buf]);     // accumulator buffer ready for promotion
+        mma_commit(&empty[s]);      // smem stage free once these MMAs have read it
+        mma_commit(&tfull[buf]);    // accumulator buffer ready for promotion
       }
     }
   } else {
-    // ---- epilogue warps: promote every stage into fp32 registers ----
+    // ---- epilogue warps: promote every stage, scaled, into fp32 registers ----
     const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
     const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
     const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
     float ar[64], ai[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
-    for (int pi = 0; pi < n_promo; ++pi) {
-      const int buf = pi & 1;
-      const uint32_t tph = (pi >> 1) & 1;
-      mbar_wait(&tfull[buf], tph);
+    for (int kc = 0; kc < nk; ++kc) {
+      const int buf = kc & 1, slot = kc % CF::SLOTS;
+      mbar_wait(&sfull[slot], (kc / CF::SLOTS) & 1);
+      mbar_wait(&tfull[buf], (kc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      const float* scs = sc + slot * (BM + BN);
+      const float sa = scs[lg * 32 + lane];
+      const float4* sbv = reinterpret_cast<const float4*>(scs + BM + ch * 64);
       const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;
 #pragma unroll
-      for (int c = 0; c < 64; c += 16) {
-        uint32_t vr[16], vi[16];
-        tmem_ld16(t_re + c, vr);
-        tmem_ld16(t_im + c, vi);
+      for (int c = 0; c < 64; c += 8) {
+        uint32_t vr[8], vi[8];
+        tmem_ld8(t_re + c, vr);
+        tmem_ld8(t_im + c, vi);
+        const float4 s0 = sbv[c / 4], s1 = sbv[c / 4 + 1];
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const float sbl[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          ar[c + j] = __fadd_rn(ar[c + j], __uint_as_float(vr[j]));
-          ai[c + j] = __fadd_rn(ai[c + j], __uint_as_float(vi[j]));
+        for (int j = 0; j < 8; ++j) {
+          const float s = sa * sbl[j];
+          ar[c + j] = __fmaf_rn(__uint_as_float(vr[j]), s, ar[c + j]);
+          ai[c + j] = __fmaf_rn(__uint_as_float(vi[j]), s, ai[c + j]);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) { mbar_arrive(&tempty[buf]); mbar_arrive(&sempty[slot]); }
     }
     // single split: write C; several: this split's fp32 partial (reduced in fp64 later)
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);

@@ -162,14 +162,14 @@ EncodeFn encode_fn() {
   }
   return fn;
 }
-// packed operand planes [b][plane][rows][K] bf16; a box = BK x box_rows x all planes
+// packed operand planes [b][plane][rows][K] fp16; a box = BK x box_rows x all planes
 CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int box_rows, int planes) {
   CUtensorMap m;
   cuuint64_t dims[3] = {cuuint64_t(1) << k_bits, cuuint64_t(1) << r_bits, cuuint64_t(planes) << nb_bits};
   cuuint64_t strides[2] = {(cuuint64_t(1) << k_bits) * 2, (cuuint64_t(1) << (k_bits + r_bits)) * 2};
   cuuint32_t box[3] = {(cuuint32_t)tnd::tc::BK, (cuuint32_t)box_rows, (cuuint32_t)planes};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Err(TN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -180,7 +180,7 @@ template <int BN>
 void ensure_gemm_attr() {
   static bool done = false;
   if (!done) {
-    CK(cudaFuncSetAttribute(tnd::tc::cgemm_bf16x6_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(tnd::tc::cgemm_f16x2s_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tnd::tc::Cfg<BN>::SMEM));
     done = true;
   }
@@ -190,7 +190,7 @@ void ensure_gemm_attr() {
 constexpr int KC_PER_SPLIT = 4096 / tnd::tc::BK;   // <= 4096 terms per TMEM accumulation
 
 struct TcStep {
-  int kind = 0;                   // 0: complex64 bf16x6 tcgen05; 1: complex128 DMMA
+  int kind = 0;                   // 0: complex64 block-scaled fp16x2 tcgen05; 1: complex128 DMMA
   PackDesc px, py;
   int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
   int64_t p_off = 0;              // split-K partials (arena offset), S > 1 only
@@ -215,6 +215,9 @@ struct Marks {
     v.push_back({e, cat});
   }
 };
+
+// bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
+int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_bits + d.k_bits); }
 
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                  Marks* mk) {
@@ -246,10 +249,13 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
   if (t.kind == 1) return launch_dmma(t, arena, ptrs_d, tab_d, st, mk);
   auto pack = [&](const PackDesc& d, int64_t off, int64_t base) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
-    tnd::pack_bf16x3_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
-        ptrs_d, d, tab_d, reinterpret_cast<__nv_bfloat16*>(arena + off), base);
+    tnd::pack_f16x2s_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
+        ptrs_d, d, tab_d, reinterpret_cast<__half*>(arena + off),
+        reinterpret_cast<float*>(arena + off + plane_bytes(d)), base);
     g_launches++;
   };
+  const float* sca = reinterpret_cast<const float*>(arena + t.x_off + plane_bytes(t.px));
+  const float* scb = reinterpret_cast<const float*>(arena + t.y_off + plane_bytes(t.py));
   const int64_t tiles = (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN) * (((int64_t(1) << t.m_bits) + 127) / 128);
   dim3 grid((unsigned)tiles, 1, (unsigned)((1u << t.nb_bits) * t.S));
   float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
@@ -261,13 +267,13 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
     const int acc = s > 0;
     if (t.BN == 128) {
       ensure_gemm_attr<128>();
-      tnd::tc::cgemm_bf16x6_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
-          t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+      tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
           partial, acc);
     } else {
       ensure_gemm_attr<64>();
-      tnd::tc::cgemm_bf16x6_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
-          t.ta, t.tb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+      tnd::tc::cgemm_f16x2s_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
           partial, acc);
     }
     g_launches++;
@@ -329,7 +335,7 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
 }
 
 // Pack descriptor: bit permutation from the operand's stored layout to [b][rows][k]
-// (destination planes [b][6][rows][k]); see pack_bf16x3_kernel.
+// (destination planes [b][planes][rows][k]); see pack_f16x2s_kernel / pack_f64x2_kernel.
 // k_lo < k bits: only the lowest k_lo bits of the k group are packed (a K-slab); the
 // source offsets of the remaining high k bits, one per slab, are appended to `slabs`.
 PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
@@ -382,7 +388,8 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   for (int j = 0; j < std::min(6, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
   for (int j = 0; j < D; ++j) if (pi[j] < 5 && !inT[j]) { inT[j] = 1; ++t; }
   for (int j = 0; j < D && t < std::min(tnd::PACK_MAX_T, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
-  if (t < 3) throw Err(TN_EUNSUPPORTED, "pack needs >= 8 elements per operand");
+  if (t < 3 || (planes == 4 && (t < 8 || k_lo < 4)))
+    throw Err(TN_EUNSUPPORTED, "tensor-core pack needs >= 256 elements and K >= 16 per operand");
   d.t_bits = t;
   int ld = 0;
   while (ld < D && inT[ld]) ++ld;
@@ -429,7 +436,11 @@ void finish_tc_kind(TcStep& t, int dtype) {
   if (t.kind == 1) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; }
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
-  return (t.kind == 1 ? int64_t(16) : int64_t(12)) << (t.nb_bits + rows_bits + t.k_lo);
+  if (t.kind == 1) return int64_t(16) << (t.nb_bits + rows_bits + t.k_lo);
+  // 4 fp16 planes + one fp32 scale per row and 32-wide K chunk (+ slack: the GEMM's
+  // scale copies read whole 128-row / BN-column tiles)
+  return (int64_t(8) << (t.nb_bits + rows_bits + t.k_lo)) +
+         (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - 5, 0))) + 1024;
 }
 
 // first-fit offsets for (size, [lo, hi]) items
@@ -663,8 +674,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       finish_tc_shape(t);
       t.c_node = c;
       finish_tc_kind(t, P.dtype);
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_y);
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_y);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -808,8 +819,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   }
   for (auto& t : P.tcs) {
     if (t.kind == 1) continue;
-    t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 6);
-    t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.BN, 6);
+    t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 4);
+    t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.BN, 4);
   }
 
   // ---- uploads ----
@@ -876,7 +887,7 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
         pr.n_gemm += t.kind ? 1 : t.n_slabs;
         pr.n_pack += 2 * (t.kind ? 1 : t.n_slabs);
         pr.flops_gemm += t.flops;
-        pr.bytes_pack += (t.kind ? 24.0 : 20.0) * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
+        pr.bytes_pack += (t.kind ? 24.0 : 16.125) * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
                                                    std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits));
       }
     }
@@ -1224,8 +1235,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       finish_tc_shape(t);
       finish_tc_kind(t, dtype);
       t.c_node = 2;
-      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 6, t.k_lo, &t.slab_y);
+      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_y);
       size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
@@ -1235,8 +1246,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
       if (t.kind == 0) {
-        t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 6);
-        t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.BN, 6);
+        t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 4);
+        t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.BN, 4);
       }
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies

@@ -1,0 +1,8 @@
+# iteration check: tc tests, all gpu tests, prof_gemm timings, bench
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 300 python -m pytest tests/test_gpu.py -x -q -k "tensor_core or tc_matches or k_slabs" 2>&1 | tail -15
+timeout 900 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -15
+for s in "13 13 12" "12 12 14" "14 14 10"; do timeout 120 python scripts/prof_gemm.py $s; done
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
+cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err

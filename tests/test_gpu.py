@@ -2,11 +2,12 @@
 
 Tolerances (DESIGN.md "Tolerances"):
   * step level, complex128 (CUDA-core DFMA): |C - C_ref| <= 1e-12 * sum_k |A||B|
-  * step level, complex64 (bf16x6 tensor cores / fp32 FMA):
+  * step level, complex64 (block-scaled fp16x2 tensor cores / fp32 FMA):
         |C - C_ref| <= (4 + 2 sqrt(K)) 2^-24 * sum_k |A||B|
-    (fp32 storage of A and B: 2 x 2^-24 per product; bf16x6 drops the x_i y_j terms
-    with i + j > 2: < 2 x 2^-24; sequential fp32 accumulation over K terms: a random
-    walk of ~sqrt(K) roundings of 2^-24, with a factor 2 margin)
+    (fp32 storage of A and B: 2 x 2^-24 per product; the fp16x2 split represents each
+    scaled element to <= 2^-24 |x| + 2^-39 max|chunk| and drops x1 y1 <= 2^-24 |x y|;
+    sequential fp32 accumulation over K terms: a random walk of ~sqrt(K) roundings of
+    2^-24, with a factor 2 margin)
   * amplitudes: complex128 |a - a_ref| <= 1e-10 * max(|a_ref|, 2^{-n/2});
     complex64 |a - a_ref| <= 1e-5 * max(|a_ref|, 2^{-n/2})  (BASELINE north_star, with the
     RMS amplitude 2^{-n/2} as the scale for amplitudes near zero)
