@@ -5,7 +5,7 @@
 //   C[b][m][n] = sum_k A[b][m][k] * B[b][k][n].
 //
 // Precision scheme: every fp32 component x of A and B
-// is scaled by a power of two per (row, 32-element K chunk) so the chunk maximum lies
+// is scaled by a power of two per (row, 64-element K chunk) so the chunk maximum lies
 // just below 2^14, then split into two fp16 pieces x = x0 + x1 (x0 = fp16(x),
 // x1 = fp16(x - x0)): 22 significand bits, the representation error is
 // <= 2^-24 |x| + 2^-39 max|chunk|.  The three products x0 y0, x0 y1, x1 y0 are
@@ -59,12 +59,12 @@ constexpr int PACK_PER_THREAD = (1 << PACK_MAX_T) / PACK_THREADS;   // 8
 // for the 16-byte loads of phase 2.
 __device__ __forceinline__ int pack_slot(int q) { return q ^ ((((q >> 4) ^ (q >> 7) ^ (q >> 10)) & 7) << 1); }
 
-// Block scaling: every chunk of SCALE_CHUNK consecutive K
+// Block scaling: every chunk of 2^SCALE_LOG2 consecutive K
 // elements of one row (re and im together) gets a power-of-two scale 2^(e-14), e the
 // exponent with max|x| < 2^e, so the scaled chunk lies in (-2^14, 2^14): the top of the
 // fp16 range, which keeps the second piece of elements far below the chunk maximum out
 // of the fp16 subnormals (absolute floor 2^-25 * 2^-14 of the chunk maximum).
-constexpr int SCALE_CHUNK = 32;
+constexpr int SCALE_LOG2 = 6;   // 64-element K chunks = 2 GEMM stages per TMEM promotion
 
 // split two scaled floats into two fp16x2 pieces: hi = fp16(x), lo = fp16(x - hi)
 __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_t& p1) {
@@ -76,9 +76,9 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 }
 
 // out planes, layout [b][4][r][k] fp16, plane = 2 * piece + {0: re, 1: im}; scales
-// [b][K / 32][r] fp32 (one per row and 32-element K chunk; one per row if K < 32).
+// [b][K / 64][r] fp32 (one per row and 64-element K chunk; one per row if K < 64).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
-// inside the tile, so every K chunk is held by 2 or 4 adjacent threads of one warp.
+// inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
 __global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* c
   const int64_t lmask = (int64_t(1) << d.ld) - 1;
   const int T = 1 << d.t_bits;
   const int RK = d.r_bits + d.k_bits;
-  const int chunk_log2 = min(d.k_bits, 5);             // log2 elements per scale
-  const int nch_log2 = max(d.k_bits - 5, 0);           // log2 chunks per row
+  const int chunk_log2 = min(d.k_bits, SCALE_LOG2);    // log2 elements per scale
+  const int nch_log2 = max(d.k_bits - SCALE_LOG2, 0);  // log2 chunks per row
   int64_t so[PACK_PER_THREAD];
   int sl[PACK_PER_THREAD];
 #pragma unroll
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* c
     for (int p = 0; p < 4; ++p) *reinterpret_cast<uint4*>(out + db + p * d.plane) = o[p];
     if ((threadIdx.x & ((1 << (chunk_log2 - 3)) - 1)) == 0) {
       const int64_t bb = db >> (RK + 2), rk = db & (d.plane - 1);
-      const int64_t r = rk >> d.k_bits, kc = (rk & ((int64_t(1) << d.k_bits) - 1)) >> 5;
+      const int64_t r = rk >> d.k_bits, kc = (rk & ((int64_t(1) << d.k_bits) - 1)) >> SCALE_LOG2;
       scales[(((bb << nch_log2) + kc) << d.r_bits) + r] = ldexpf(1.f, e - 14);
     }
   }
@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* c
 namespace tc {
 
 constexpr int BM = 128;    // rows per tile (TMEM lanes)
-constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B) = one scale chunk
+constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
+constexpr int PROMO = 2;   // stages per TMEM accumulation = one 64-element scale chunk
 constexpr int GROUP_M = 8; // CTA rasterization: 8 M-tiles share each B panel in flight
 
 template <int BN>
@@ -200,6 +201,16 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 // plain bulk copy global -> shared (16-byte aligned, size a multiple of 16)
 __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -244,10 +255,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // Complex GEMM C[b][m][n] (+)= sum_k A[b][m][k] B[b][n][k] on block-scaled fp16x2
 // operands.  Per 32-wide K stage the MMA warp issues
-// 2 (k16) x 3 piece pairs (hi.hi, hi.lo, lo.hi) x 4 real products = 24 MMAs into a fresh
-// TMEM buffer; the epilogue warps promote it into fp32 registers, multiplying by the
-// stage's chunk scales sA[row] * sB[col] (round-to-nearest; tcgen05 fp32 accumulation
-// truncates, so no accumulator sees more than 12 updates).  Two TMEM buffers ping-pong.
+// 2 (k16) x 3 piece pairs (hi.hi, hi.lo, lo.hi) x 4 real products = 24 MMAs; every
+// 2 stages (one 64-wide scale chunk) go into a fresh TMEM buffer, which the epilogue
+// warps promote into fp32 registers, multiplying by the chunk scales sA[row] * sB[col]
+// (round-to-nearest; tcgen05 fp32 accumulation truncates, so no accumulator sees more
+// than 24 updates).  Two TMEM buffers ping-pong.
 template <int BN>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -281,6 +293,8 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   const int nk_all = (K + BK - 1) / BK;
   const int kc0 = split * kc_per_split;
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+  const int nch_all = (nk_all + PROMO - 1) / PROMO;     // scale chunks of the whole K
+  const int n_promo = (nk + PROMO - 1) / PROMO;
 
   if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -302,9 +316,17 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 
   if (warp == TMA_WARP) {
     if (lane == 0) {
-      const float* sa = scA + ((int64_t)b * nk_all) * M + m_blk * BM;
-      const float* sb = scB + ((int64_t)b * nk_all) * N + n_blk * BN;
+      const float* sa = scA + ((int64_t)b * nch_all) * M + m_blk * BM;
+      const float* sb = scB + ((int64_t)b * nch_all) * N + n_blk * BN;
       for (int kc = 0; kc < nk; ++kc) {
+        if (kc % PROMO == 0) {                  // chunk scales of this promotion
+          const int pi = kc / PROMO, slot = pi % CF::SLOTS, cg = (kc0 + kc) / PROMO;
+          mbar_wait(&sempty[slot], ((pi / CF::SLOTS) & 1) ^ 1);
+          mbar_expect_tx(&sfull[slot], CF::SC_BYTES);
+          float* d = sc + slot * (BM + BN);
+          bulk_load(d, sa + (int64_t)cg * M, BM * 4, &sfull[slot]);
+          bulk_load(d + BM, sb + (int64_t)cg * N, BN * 4, &sfull[slot]);
+        }
         const int s = kc % CF::STAGES;
         const uint32_t ph = (kc / CF::STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
@@ -312,12 +334,6 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
         uint8_t* st = smem + s * CF::STAGE;
         tma_load_3d(&tmA, st, &full[s], (kc0 + kc) * BK, m_blk * BM, b * 4);               // 4 planes
         tma_load_3d(&tmB, st + CF::A_BYTES, &full[s], (kc0 + kc) * BK, n_blk * BN, b * 4); // 4 planes
-        const int slot = kc % CF::SLOTS;
-        mbar_wait(&sempty[slot], ((kc / CF::SLOTS) & 1) ^ 1);
-        mbar_expect_tx(&sfull[slot], CF::SC_BYTES);
-        float* d = sc + slot * (BM + BN);
-        bulk_load(d, sa + (int64_t)(kc0 + kc) * M, BM * 4, &sfull[slot]);
-        bulk_load(d + BM, sb + (int64_t)(kc0 + kc) * N, BN * 4, &sfull[slot]);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -330,8 +346,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % CF::STAGES;
         const uint32_t ph = (kc / CF::STAGES) & 1;
-        const int buf = kc & 1;
-        mbar_wait(&tempty[buf], ((kc >> 1) & 1) ^ 1);   // epilogue drained this buffer
+        const int pi = kc / PROMO;
+        const int buf = pi & 1;
+        const bool first = (kc % PROMO) == 0;
+        const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
+        if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // epilogue drained this buffer
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
@@ -344,7 +363,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
             const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
             const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
             const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint32_t acc = ((ks | q) == 0) ? 0u : 1u;   // fresh accumulator per stage
+            const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;   // fresh accumulator per promotion
             mma_f16(t_re, a_re, b_re, idesc, acc);
             mma_f16(t_re, a_im, b_im, idesc_negA, 1u);
             mma_f16(t_im, a_re, b_im, idesc, acc);
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
           }
         }
         mma_commit(&empty[s]);      // smem stage free once these MMAs have read it
-        mma_commit(&tfull[buf]);    // accumulator buffer ready for promotion
+        if (last) mma_commit(&tfull[buf]);    // accumulator buffer ready for promotion
       }
     }
   } else {
@@ -363,21 +382,21 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     float ar[64], ai[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
-    for (int kc = 0; kc < nk; ++kc) {
-      const int buf = kc & 1, slot = kc % CF::SLOTS;
-      mbar_wait(&sfull[slot], (kc / CF::SLOTS) & 1);
-      mbar_wait(&tfull[buf], (kc >> 1) & 1);
+    for (int pi = 0; pi < n_promo; ++pi) {
+      const int buf = pi & 1, slot = pi % CF::SLOTS;
+      mbar_wait(&sfull[slot], (pi / CF::SLOTS) & 1);
+      mbar_wait(&tfull[buf], (pi >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const float* scs = sc + slot * (BM + BN);
-      const float sa = scs[lg * 32 + lane];
-      const float4* sbv = reinterpret_cast<const float4*>(scs + BM + ch * 64);
+      const uint32_t scs = smem_u32(sc + slot * (BM + BN));
+      const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
+      const uint32_t sbv = scs + 4 * (BM + ch * 64);
       const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;
 #pragma unroll
       for (int c = 0; c < 64; c += 8) {
         uint32_t vr[8], vi[8];
         tmem_ld8(t_re + c, vr);
         tmem_ld8(t_im + c, vi);
-        const float4 s0 = sbv[c / 4], s1 = sbv[c / 4 + 1];
+        const float4 s0 = lds_f32x4(sbv + 4 * c), s1 = lds_f32x4(sbv + 4 * c + 16);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const float sbl[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll

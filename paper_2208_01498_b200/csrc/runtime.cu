@@ -437,10 +437,10 @@ void finish_tc_kind(TcStep& t, int dtype) {
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
   if (t.kind == 1) return int64_t(16) << (t.nb_bits + rows_bits + t.k_lo);
-  // 4 fp16 planes + one fp32 scale per row and 32-wide K chunk (+ slack: the GEMM's
+  // 4 fp16 planes + one fp32 scale per row and 64-wide K chunk (+ slack: the GEMM's
   // scale copies read whole 128-row / BN-column tiles)
   return (int64_t(8) << (t.nb_bits + rows_bits + t.k_lo)) +
-         (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - 5, 0))) + 1024;
+         (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - 6, 0))) + 1024;
 }
 
 // first-fit offsets for (size, [lo, hi]) items

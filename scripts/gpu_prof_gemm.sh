@@ -1,0 +1,7 @@
+# ncu --set full of the tensor-core GEMM on one config-1-like step (m=n=2^13, K=2^12)
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+python scripts/prof_gemm.py 13 13 12 > gpurun_out/prof_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:cgemm -s 2 -c 1 -o gpurun_out/prof_cgemm python scripts/prof_gemm.py 13 13 12 > gpurun_out/ncu_cgemm.log 2>&1
+echo ncu_rc=$?
+cat gpurun_out/prof_plain.log; tail -3 gpurun_out/ncu_cgemm.log

@@ -45,13 +45,14 @@ def c64_tol(K):
     return (4.0 + 2.0 * math.sqrt(K)) * 2.0 ** -24
 
 
-def _run_pair(inds_a, inds_b, inds_c, dims, dtype, path, seed=0):
+def _run_pair(inds_a, inds_b, inds_c, dims, dtype, path, seed=0, gen=None):
     dev = _cuda()
     sa = [dims[i] for i in inds_a]
     sb = [dims[i] for i in inds_b]
     sc = [dims[i] for i in inds_c]
-    A = _rand(sa, seed, dtype)
-    B = _rand(sb, seed + 1, dtype)
+    gen = gen or _rand
+    A = gen(sa, seed, dtype)
+    B = gen(sb, seed + 1, dtype)
     tdt = torch.complex64 if dtype == tb.TN_C64 else torch.complex128
     tA = torch.from_numpy(A).to(dev)
     tB = torch.from_numpy(B).to(dev)
@@ -124,6 +125,46 @@ def test_pair_tensor_core_path(case):
     got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=10 + case)
     err = np.abs(got - ref)
     assert np.all(err <= c64_tol(2 ** k) * bound + 1e-30), (err / bound).max()
+
+
+def _wide_range(shape, seed, dtype):
+    """complex Gaussian entries times 2^u, u uniform in [-24, 24] per entry, with some
+    exact zeros and a few entries scaled by 1e-25 / 1e+6 (products stay finite in
+    complex64): the block-scaled fp16x2 split
+    must stay at fp32 level relative to sum_k |A||B|."""
+    g = np.random.default_rng(seed)
+    x = _rand(shape, seed, dtype).astype(np.complex128)
+    x = x * np.exp2(g.uniform(-24, 24, shape))
+    flat = x.reshape(-1)
+    idx = g.permutation(flat.size)
+    flat[idx[: flat.size // 16]] = 0
+    flat[idx[flat.size // 16: flat.size // 16 + 8]] *= 1e-25
+    flat[idx[flat.size // 16 + 8: flat.size // 16 + 12]] *= 1e+6
+    return x.astype(np.complex64 if dtype == tb.TN_C64 else np.complex128)
+
+
+@pytest.mark.parametrize("case", [(0, 7, 8, 9, None), (1, 6, 7, 13, 7), (0, 7, 7, 4, 1)])
+def test_pair_tensor_core_wide_dynamic_range(case):
+    nb, m, n, k, ps = case
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=40, gen=_wide_range)
+    err = np.abs(got - ref)
+    assert np.all(np.isfinite(got))
+    assert np.all(err <= c64_tol(2 ** k) * bound + 1e-38), (err / np.maximum(bound, 1e-300)).max()
+
+
+def _zero_chunks(shape, seed, dtype):
+    """Gaussian entries with every other run of 64 consecutive elements set to zero."""
+    x = _rand(shape, seed, dtype).reshape(-1).copy()
+    for j in range(0, x.size, 128):
+        x[j:j + 64] = 0
+    return x.reshape(shape)
+
+
+def test_pair_tensor_core_zero_chunks():
+    ia, ib, ic, dims = _gemm_case(0, 7, 7, 8, None)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=41, gen=_zero_chunks)
+    assert np.all(np.abs(got - ref) <= c64_tol(2 ** 8) * bound + 1e-30)
 
 
 DMMA_CASES = [
