@@ -200,7 +200,7 @@ def run_ours(args):
     flops_slice = float(pinfo["flops_per_slice"])
     my_bits = bits[rank::ws]
     bits_dev = torch.from_numpy(np.ascontiguousarray(my_bits[0])).to(dev)
-    amp = torch.zeros(1, dtype=torch.complex64, device=dev)
+    amp = torch.zeros(1, dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 

@@ -120,7 +120,8 @@ typedef struct {
   int32_t median_fallbacks;
   double log2_total_2M;                 /* log2 sum_k 2 M_k, unsliced (Eq. (3)) */
   double log2_slice_2M;                 /* log2 sum_k 2 M_k of one slice */
-  int64_t n_slice_assignments;          /* prod of sliced dimensions */
+  int64_t n_slice_assignments;          /* prod of sliced dimensions, saturated at INT64_MAX */
+  int32_t slice_bits;                   /* log2 n_slice_assignments (exact) */
 } tn_order_info;
 int tn_order_get_info(tn_order ord, tn_order_info* info);
 /* steps: host int32[2 * n_steps] (a, b) pairs; leaves are tensor ids 0..n-1 and
@@ -140,10 +141,13 @@ void tn_plan_free(tn_plan plan);
 
 typedef struct {
   double flops_per_slice;        /* 8 * sum_k M_k (real flops of complex MACs) */
-  int64_t n_slices;              /* slice assignments */
+  int64_t n_slices;              /* slice assignments, saturated at INT64_MAX: with more than
+                                    63 sliced bits only slice ids < 2^63 are addressable (their
+                                    higher sliced bits are 0) */
   int64_t arena_bytes;           /* device arena size */
   int32_t n_steps_small, n_steps_tc, n_launches_per_slice;
   double tc_flops_per_slice;     /* part of flops_per_slice on the tensor-core path */
+  int32_t slice_bits;            /* log2 of the number of slice assignments */
 } tn_plan_info;
 int tn_plan_get_info(tn_plan plan, tn_plan_info* info);
 
@@ -158,7 +162,10 @@ int tn_plan_steps(tn_plan plan, int32_t* out);
 int tn_contract(tn_plan plan, const uint8_t* bits, int64_t slice_begin, int64_t slice_end,
                 double* amp, void* stream);
 /* tn_contract_device: same, asynchronous; bits_dev: device uint8[n_qubits];
- * amp_dev: device complex (plan dtype) accumulator, the sum is ADDED to it. */
+ * amp_dev: device complex128 accumulator (2 doubles, any plan dtype), the sum is ADDED
+ * to it.  Slices are summed in fp64; the plan's power-of-two leaf scaling (DESIGN.md
+ * "Range") is undone in fp64 at that sum, so slices far below the complex64 range of
+ * the intermediates still contribute exactly as computed. */
 int tn_contract_device(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin,
                        int64_t slice_end, void* amp_dev, void* stream);
 /* tn_contract_profiled: as tn_contract_device, but launches eagerly (no graph) with

@@ -87,30 +87,39 @@ def contract_pair(Ainds, A, Binds, B, kept, dims):
     return out, np.array(C, order="C", copy=True)
 
 
+def contract_slice(net, steps, bits, fixed, kept=None, keep_intermediates=False):
+    """One sliced sub-contraction ("index slicing"): the closed network
+    with the output legs bound to `bits` and every sliced index i fixed to fixed[i],
+    contracted along `steps`; returns the scalar (and the intermediates if asked)."""
+    kept = kept if kept is not None else kept_per_step(net, steps)
+    n = len(net.tensors)
+    nodes = dict(enumerate(leaf_tensors(net, bits, fixed)))
+    inter = [] if keep_intermediates else None
+    for k, (a, b) in enumerate(steps):
+        (Ai, A), (Bi, B) = nodes.pop(a), nodes.pop(b)
+        kk = [i for i in kept[k] if i not in fixed]
+        nodes[n + k] = contract_pair(Ai, A, Bi, B, kk, net.dims)
+        if keep_intermediates:
+            inter.append(nodes[n + k])
+    val = 1.0 + 0j
+    for inds, data in nodes.values():     # a single root, or disconnected pieces
+        assert not inds
+        val *= complex(data)
+    return (val, inter) if keep_intermediates else val
+
+
 def contract_tree(net, steps, bits, sliced=(), keep_intermediates=False):
     """<x|C|0> by contracting the closed network along `steps`; sliced indices are
     summed outside the tree (every assignment contracted separately and added)."""
     kept = kept_per_step(net, steps)
-    n = len(net.tensors)
     sliced = list(sliced)
     total = 0j
     inter = None
     for vals in itertools.product(*[range(net.dims[i]) for i in sliced]):
-        fixed = dict(zip(sliced, vals))
-        nodes = dict(enumerate(leaf_tensors(net, bits, fixed)))
+        r = contract_slice(net, steps, bits, dict(zip(sliced, vals)), kept, keep_intermediates)
         if keep_intermediates:
-            inter = []
-        for k, (a, b) in enumerate(steps):
-            (Ai, A), (Bi, B) = nodes.pop(a), nodes.pop(b)
-            kk = [i for i in kept[k] if i not in fixed]
-            nodes[n + k] = contract_pair(Ai, A, Bi, B, kk, net.dims)
-            if keep_intermediates:
-                inter.append(nodes[n + k])
-        val = 1.0 + 0j
-        for inds, data in nodes.values():     # a single root, or disconnected pieces
-            assert not inds
-            val *= complex(data)
-        total += val
+            r, inter = r
+        total += r
     return (total, inter) if keep_intermediates else total
 
 

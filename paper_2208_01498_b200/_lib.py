@@ -39,7 +39,7 @@ class _OrderInfo(C.Structure):
     _fields_ = [("n_steps", C.c_int32), ("n_slices", C.c_int32), ("max_step_log2", C.c_int32),
                 ("max_size_log2", C.c_int32), ("median_fallbacks", C.c_int32),
                 ("log2_total_2M", C.c_double), ("log2_slice_2M", C.c_double),
-                ("n_slice_assignments", C.c_int64)]
+                ("n_slice_assignments", C.c_int64), ("slice_bits", C.c_int32)]
 
 
 class Profile(C.Structure):
@@ -52,7 +52,7 @@ class Profile(C.Structure):
 class _PlanInfo(C.Structure):
     _fields_ = [("flops_per_slice", C.c_double), ("n_slices", C.c_int64), ("arena_bytes", C.c_int64),
                 ("n_steps_small", C.c_int32), ("n_steps_tc", C.c_int32), ("n_launches_per_slice", C.c_int32),
-                ("tc_flops_per_slice", C.c_double)]
+                ("tc_flops_per_slice", C.c_double), ("slice_bits", C.c_int32)]
 
 
 def _load():

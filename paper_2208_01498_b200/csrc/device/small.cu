@@ -93,24 +93,24 @@ __global__ void set_leaf_ptrs_kernel(void** __restrict__ ptrs, const int64_t* __
     if (k >= 0) val = bits[k];
     else {
       int j = -1 - k;
-      val = (s >> slice_shift[j]) & ((int64_t(1) << slice_dim_log2[j]) - 1);
+      // slice ids are int64: sliced bits at positions >= 63 are 0 (tn.h, tn_plan_info)
+      val = slice_shift[j] >= 63 ? 0 : (s >> slice_shift[j]) & ((int64_t(1) << slice_dim_log2[j]) - 1);
     }
     off += val * var_stride[v];
   }
   ptrs[t] = arena_leaves + off * elem_bytes;
 }
 
-// amp += root scalar; advance the slice counter (one thread)
+// amp (complex128) += root scalar * 2^root_exp (undoes the plan's leaf scaling, in
+// fp64); advance the slice counter (one thread)
 template <typename R>
-__global__ void accumulate_root_kernel(const void* const* __restrict__ ptrs, int32_t root,
-                                       void* __restrict__ amp, int64_t* __restrict__ slice_id) {
+__global__ void accumulate_root_kernel(const void* const* __restrict__ ptrs, int32_t root, int32_t root_exp,
+                                       double2* __restrict__ amp, int64_t* __restrict__ slice_id) {
   using C2 = typename cplx_t<R>::type;
   const C2 v = *reinterpret_cast<const C2*>(ptrs[root]);
-  C2* a = reinterpret_cast<C2*>(amp);
-  a->x += v.x;
-  a->y += v.y;
+  amp->x += ldexp((double)v.x, root_exp);
+  amp->y += ldexp((double)v.y, root_exp);
   *slice_id += 1;
 }
-
 
 }  // namespace tnd

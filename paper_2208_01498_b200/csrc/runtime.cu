@@ -492,6 +492,7 @@ struct tn_plan_s {
   std::vector<TcStep> tcs;
   std::vector<std::pair<int, int>> launches;  // (0, wave) | (1, tc)
   int64_t n_slices = 1;
+  int slice_bits = 0;
   double flops = 0, tc_flops = 0;
   int n_small = 0;
   // device
@@ -508,7 +509,8 @@ struct tn_plan_s {
   int32_t* sl_shift_d = nullptr;
   uint8_t* bits_d = nullptr;
   int64_t* slice_d = nullptr;
-  void* amp_d = nullptr;
+  double2* amp_d = nullptr;      // complex128 accumulator of one contraction
+  int root_exp = 0;              // the root carries 2^-root_exp of leaf scaling
   cudaStream_t cap = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t kernels_per_slice = 0;
@@ -529,8 +531,8 @@ struct tn_plan_s {
         k += tcs[L.second].kind ? 3 : tcs[L.second].n_slabs * (tcs[L.second].S > 1 ? 4 : 3);
       }
     }
-    if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
-    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_d, root, amp_d, slice_d);
+    if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
     CK(cudaGetLastError());
     kernels_per_slice = k + 1;
   }
@@ -541,7 +543,7 @@ struct tn_plan_s {
     for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
     for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
                     (void*)var_kind_d, (void*)var_stride_d, (void*)sl_log2_d, (void*)sl_shift_d, (void*)bits_d,
-                    (void*)slice_d, amp_d})
+                    (void*)slice_d, (void*)amp_d})
       if (p) cudaFree(p);
   }
 };
@@ -549,13 +551,9 @@ struct tn_plan_s {
 namespace {
 
 __global__ void set_i64_kernel(int64_t* p, int64_t v) { *p = v; }
-template <typename R>
-__global__ void add_amp_kernel(void* dst, const void* src) {
-  using C2 = typename tnd::cplx_t<R>::type;
-  C2* d = reinterpret_cast<C2*>(dst);
-  const C2* s = reinterpret_cast<const C2*>(src);
-  d->x += s->x;
-  d->y += s->y;
+__global__ void add_amp_kernel(double2* dst, const double2* src) {
+  dst->x += src->x;
+  dst->y += src->y;
 }
 
 template <typename T>
@@ -599,10 +597,22 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   std::vector<int32_t> var_begin(n + 1, 0), var_kind;
   std::vector<char> leaf_host;
   int64_t leaf_elems = 0;
+  // Leaf scaling: binding an output leg or fixing a sliced index
+  // bit shrinks the contraction by ~2^-1/2, so a sliced amplitude of many qubits
+  // leaves the complex64 exponent range (config 4 slices reach 2^-165).  Leaf t is
+  // scaled by 2^c_t, c_t the integer steps of a running sum of half a bit per bound
+  // leg / sliced bit it holds; the root is multiplied by 2^-sum c_t in fp64.
+  int half_bits = 0, scale_exp = 0;
   for (int t = 0; t < n; ++t) {
     const auto& T = net.tensors[t];
     std::vector<int> vars, rest;
     for (int i : T.inds) (out_q.count(i) || sliced.count(i) ? vars : rest).push_back(i);
+    int bound = 0;
+    for (int i : vars) bound += out_q.count(i) ? 1 : l2[i];
+    const int c_t = (half_bits + bound) / 2 - half_bits / 2;
+    half_bits += bound;
+    scale_exp += c_t;
+    const double leaf_scale = std::ldexp(1.0, c_t);
     L[t].inds = rest;
     L[t].bits = sum_bits(rest, l2);
     std::vector<int> ninds = vars;
@@ -633,7 +643,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
         size_t pos = std::find(T.inds.begin(), T.inds.end(), ninds[k]) - T.inds.begin();
         src += st[pos] * dig[k];
       }
-      const tn::cplx z = T.data[src];
+      const tn::cplx z = T.data[src] * leaf_scale;
       if (P.dtype == TN_C64) {
         float v[2] = {(float)z.real(), (float)z.imag()};
         std::memcpy(&leaf_host[off + it * 8], v, 8);
@@ -648,6 +658,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     leaf_elems += pad;
     leaf_host.resize((size_t)leaf_elems * P.esz, 0);
   }
+
+  P.root_exp = -scale_exp;
 
   // ---- steps ----
   auto kept_all = tn::kept_per_step(net, ord.steps);
@@ -835,7 +847,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   int sh = 0;
   for (int j = (int)ord.slices.size() - 1; j >= 0; --j) { sl_shift[j] = sh; sh += l2[ord.slices[j]]; }
   for (int i : ord.slices) sl_log2.push_back(l2[i]);
-  P.n_slices = int64_t(1) << sh;
+  P.slice_bits = sh;
+  P.n_slices = sh >= 63 ? INT64_MAX : int64_t(1) << sh;
   P.sl_log2_d = upload(sl_log2);
   P.sl_shift_d = upload(sl_shift);
   CK(cudaMalloc(&P.bits_d, std::max(1, net.n_qubits)));
@@ -892,8 +905,8 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
       }
     }
     mk.mark(st, 4);
-    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
-    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.amp_d, P.slice_d);
+    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
     g_launches++;
     pr.n_other++;
     mk.mark(st, -1);
@@ -1029,8 +1042,9 @@ int tn_order_get_info(tn_order o, tn_order_info* info) {
     std::vector<std::vector<int>> node(n + od.steps.size());
     for (int t = 0; t < n; ++t) node[t] = o->net->closed_inds(t);
     double w = 0;
-    int64_t nsl = 1;
-    for (int i : od.slices) nsl *= o->net->dims[i];
+    int sbits = 0;
+    for (int i : od.slices) sbits += o->net->log2dim(i);
+    const int64_t nsl = sbits >= 63 ? INT64_MAX : int64_t(1) << sbits;
     for (size_t k = 0; k < od.steps.size(); ++k) {
       std::set<int> u(node[od.steps[k].first].begin(), node[od.steps[k].first].end());
       u.insert(node[od.steps[k].second].begin(), node[od.steps[k].second].end());
@@ -1041,6 +1055,7 @@ int tn_order_get_info(tn_order o, tn_order_info* info) {
     }
     info->log2_slice_2M = w > 0 ? std::log2(w) : 0;
     info->n_slice_assignments = nsl;
+    info->slice_bits = sbits;
   });
 }
 int tn_order_steps(tn_order o, int32_t* steps) {
@@ -1080,6 +1095,7 @@ int tn_plan_get_info(tn_plan p, tn_plan_info* info) {
     info->n_steps_tc = (int32_t)p->tcs.size();
     info->n_launches_per_slice = (int32_t)p->kernels_per_slice;
     info->tc_flops_per_slice = p->tc_flops;
+    info->slice_bits = p->slice_bits;
   });
 }
 
@@ -1096,15 +1112,8 @@ int tn_contract(tn_plan p, const uint8_t* bits, int64_t slice_begin, int64_t sli
     cudaStream_t st = (cudaStream_t)stream;
     run_slices(*p, bits, false, slice_begin, slice_end, st);
     double h[2] = {0, 0};
-    if (p->dtype == TN_C64) {
-      float f[2];
-      CK(cudaMemcpyAsync(f, p->amp_d, 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      h[0] = f[0]; h[1] = f[1];
-    } else {
-      CK(cudaMemcpyAsync(h, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-    }
+    CK(cudaMemcpyAsync(h, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     amp[0] = h[0];
     amp[1] = h[1];
   });
@@ -1116,8 +1125,7 @@ int tn_contract_device(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin, 
     if (!p || !amp_dev || (!bits_dev && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
     cudaStream_t st = (cudaStream_t)stream;
     run_slices(*p, bits_dev, true, slice_begin, slice_end, st);
-    if (p->dtype == TN_C64) add_amp_kernel<float><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
-    else add_amp_kernel<double><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    add_amp_kernel<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(amp_dev), p->amp_d);
     g_launches++;
     CK(cudaGetLastError());
   });
@@ -1134,8 +1142,7 @@ int tn_contract_profiled(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin
     set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
     CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
     profile_slices(*p, slice_begin, slice_end, st, *prof);
-    if (p->dtype == TN_C64) add_amp_kernel<float><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
-    else add_amp_kernel<double><<<1, 1, 0, st>>>(amp_dev, p->amp_d);
+    add_amp_kernel<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(amp_dev), p->amp_d);
     g_launches++;
     CK(cudaGetLastError());
   });
@@ -1148,15 +1155,8 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
     const int nq = p->net->n_qubits;
     for (int j = 0; j < n_bits; ++j) {
       run_slices(*p, bits + (size_t)j * nq, false, 0, p->n_slices, st);
-      if (p->dtype == TN_C64) {
-        float f[2];
-        CK(cudaMemcpyAsync(f, p->amp_d, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        amps[2 * j] = f[0]; amps[2 * j + 1] = f[1];
-      } else {
-        CK(cudaMemcpyAsync(amps + 2 * j, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-      }
+      CK(cudaMemcpyAsync(amps + 2 * j, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
     }
   });
 }
