@@ -2,15 +2,21 @@
 """Benchmark of the contraction hot path (BASELINE.json metric: contraction FLOP/s and
 amplitudes/s on B200, % of tensor-pipe peak).
 
-Workload (N=1): configs[1] -- 8x8 qubit lattice, depth 16, Haar U(2) + CZ brickwork,
-complex64 on block-scaled fp16x2 split-precision tensor cores, separator order (SM Algorithm 1)
-sliced so every tensor fits HBM.  Its amplitudes are partitioned by bitstring across
-ranks (weak scaling): rank r contracts bitstrings r, r+N, ... of the seeded batch of
-1024.  One STEP = one slice of one amplitude (the whole separator tree over one
-sliced sub-network); an amplitude is n_slices steps.  Intermediates are GBs, far
-larger than the 126 MB L2, so no L2 flush is needed between steps.
+Default workload (N=1): configs[1] -- 8x8 qubit lattice, depth 16, Haar U(2) + CZ
+brickwork, complex64 on block-scaled fp16x2 split-precision tensor cores, separator
+order (SM Algorithm 1) sliced so every tensor fits HBM.  Its amplitudes are partitioned
+by bitstring across ranks (weak scaling): rank r contracts bitstrings r, r+N, ... of the
+seeded batch of 1024.  One STEP = one slice of one amplitude (the whole separator tree
+over one sliced sub-network); an amplitude is n_slices steps.  Intermediates are GBs,
+far larger than the 126 MB L2, so no L2 flush is needed between steps.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+--config 2 / 4 (Sycamore-53 m=14, (2+1)D 12x12 depth 20; complex64): one amplitude,
+its slices partitioned across ranks (rank r takes slices [r K, (r+1) K) of the K timed
+steps), the per-rank partial amplitudes summed by ONE NCCL all-reduce inside the timed
+region.  --config 3 (IQP 10x10, complex128 on the FP64 tensor pipe): one STEP = one
+full amplitude (unsliced), bitstrings r::N of 256 per rank.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C] [--impl reference]
 Prints ONE JSON line (rank 0).
 """
 from __future__ import annotations
@@ -30,9 +36,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "contraction FLOP/s"
-CONFIG_IDX = 1
-SLICE_LOGS = (34, 33, 32, 31)   # largest tensor of a slice: 2^34 complex64 = 128 GB-class plan (arena ~170 GB), else smaller
 ORDER_SEED = 0
+# per config: arithmetic type, how the units shard across ranks, slicing targets tried in
+# order (largest tensor of a slice 2^t entries; the first plan that fits HBM is used)
+SPEC = {
+    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False),
+    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False),
+    3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True),
+    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False),
+}
+# complex128 GEMM on DMMA: no measured fp64 peak on this pool -> measured bf16 sustained
+# x the B200 datasheet ratio of dense FP64 tensor (40 TF/s) to dense bf16 (2250 TF/s)
+FP64_TC_PER_BF16 = 40.0 / 2250.0
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # split-precision complex64: one complex MAC (8 useful flops) = 4 real products x 3 fp16
 # piece products (hi.hi, hi.lo, lo.hi) = 24 fp16 tensor flops; fp16 dense rate = bf16 rate
@@ -96,14 +111,14 @@ def dist_env():
     return ws, rank, local
 
 
-def workload():
-    from tn_inputs import config_circuit, random_bitstrings
-    c = config_circuit(CONFIG_IDX)
-    bits = random_bitstrings(c.n, 1024, 1)
+def workload(ci):
+    from tn_inputs import config_circuit, random_bitstrings, CONFIGS
+    c = config_circuit(ci)
+    bits = random_bitstrings(c.n, max(1, CONFIGS[ci]["n_bitstrings"]), 1)
     return c, bits
 
 
-def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=SLICE_LOGS[0]):
+def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=34, hyper=False):
     """The oracle as it stands on the host cores: slice 0 of bitstring 0 of the same
     network/order (oracle.ssa.find_order + choose_slices), contracting the steps of
     the separator tree in order with oracle.contract.contract_pair until `budget_s`
@@ -116,9 +131,9 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=SLICE_LOGS[0]):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    net = build_network(c)
+    net = build_network(c, diag_hyper=hyper)
     steps, _ = find_order(net, seed=ORDER_SEED)
-    sl = choose_slices(net, steps, slice_log2)
+    sl = choose_slices(net, steps, slice_log2) if slice_log2 > 0 else []
     kept = kept_per_step(net, steps)
     fixed = {i: 0 for i in sl}
     n = len(net.tensors)
@@ -156,16 +171,18 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    c, bits = workload()
+    spec = SPEC[args.config]
+    c, bits = workload(args.config)
     vals = []
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline_sample(c, bits, budget_s=max(2.0, 60.0 / (args.warmup + args.steps))))
+        vals.append(cpu_baseline_sample(c, bits, budget_s=max(2.0, 60.0 / (args.warmup + args.steps)),
+                                        slice_log2=spec["slice_logs"][0], hyper=spec["hyper"]))
     timed = vals[args.warmup:]
     v = float(np.mean([t["value"] for t in timed]))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "FLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": "configs[1] lattice_cz 8x8 depth 16 (oracle, bounded sample per step)"},
+            "config": {"workload": f"configs[{args.config}] {c.name} (oracle, bounded sample per step)"},
             "cpu_baseline": {"value": v, "unit": "FLOP/s", "cores": timed[0]["cores"], "kind": "oracle",
                              "sample": timed[0]["sample"]},
             "e2e": {"value": v, "unit": "FLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -183,13 +200,16 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     import paper_2208_01498_b200 as tb
 
-    c, bits = workload()
-    net = tb.Network.from_circuit(c)
+    ci = args.config
+    spec = SPEC[ci]
+    c, bits = workload(ci)
+    dtype = tb.TN_C64 if spec["dtype"] == "c64" else tb.TN_C128
+    net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
     plan = None
-    for slice_log2 in SLICE_LOGS:
+    for slice_log2 in spec["slice_logs"]:
         order = tb.Order(net, seed=ORDER_SEED, max_log2_size=slice_log2)
         try:
-            plan = tb.Plan(net, order, dtype=tb.TN_C64, device=local)
+            plan = tb.Plan(net, order, dtype=dtype, device=local)
             break
         except tb.TnError as e:       # arena does not fit this GPU: slice further
             print(f"slicing target 2^{slice_log2}: {e}", file=sys.stderr)
@@ -197,16 +217,29 @@ def run_ours(args):
         raise RuntimeError("no slicing target fits device memory")
     pinfo = plan.info()
     n_slices = int(pinfo["n_slices"])
+    slice_bits = int(pinfo["slice_bits"])
     flops_slice = float(pinfo["flops_per_slice"])
-    my_bits = bits[rank::ws]
-    bits_dev = torch.from_numpy(np.ascontiguousarray(my_bits[0])).to(dev)
+    by_slices = spec["shard"] == "slices"
+    # one step: one slice (sliced configs) or one whole amplitude (unsliced)
+    step_slices = 1 if n_slices > 1 else n_slices
+    my_bits = bits[0:1] if by_slices else bits[rank::ws]
+    bits_dev = torch.from_numpy(np.ascontiguousarray(my_bits)).to(dev)
+    nq = c.n
     amp = torch.zeros(1, dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
-    # warm-up (graph path and profiled path)
+    def step_args(j):
+        """(bitstring row, first slice) of this rank's j-th step"""
+        if by_slices:       # rank r: slices [r * K, (r + 1) * K) of one amplitude (+ warm-up offset)
+            return 0, (rank * args.steps + j) % max(n_slices, 1)
+        if n_slices > 1:    # config 1: slices of this rank's first bitstring
+            return 0, j % n_slices
+        return j % len(my_bits), 0
+
     for w in range(args.warmup):
-        plan.contract_device(bits_dev.data_ptr(), w % n_slices, w % n_slices + 1, amp.data_ptr(), sptr)
+        row, sl = step_args(args.steps + w)
+        plan.contract_device(bits_dev[row].data_ptr(), sl, sl + step_slices, amp.data_ptr(), sptr)
     torch.cuda.synchronize()
 
     def barrier():
@@ -214,18 +247,21 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- timed region: K steps (slices) through the profiled launcher ----
+    # ---- timed region: K steps through the profiled launcher (+ the slice all-reduce) ----
+    amp.zero_()
     launches0 = tb.kernel_launches()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record(stream)
         prof = {}
-        for s in range(args.steps):
-            sl = (args.warmup + s) % n_slices
-            p = plan.contract_profiled(bits_dev.data_ptr(), sl, sl + 1, amp.data_ptr(), sptr)
+        for j in range(args.steps):
+            row, sl = step_args(j)
+            p = plan.contract_profiled(bits_dev[row].data_ptr(), sl, sl + step_slices, amp.data_ptr(), sptr)
             for k, v in p.items():
                 prof[k] = prof.get(k, 0) + v
+        if by_slices and ws > 1:
+            torch.distributed.all_reduce(amp)        # partial amplitudes of all ranks' slices
         e1.record(stream)
         barrier()
     launches = tb.kernel_launches() - launches0
@@ -234,56 +270,83 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
     ms = float(t_max.item())
-    total_flops = flops_slice * args.steps * ws
+    flops_step = flops_slice * step_slices
+    total_flops = flops_step * args.steps * ws
     value = total_flops / (ms / 1e3)
-    amps_per_s = value / (flops_slice * n_slices)
+    amps_per_s = value / (flops_slice * (2.0 ** slice_bits))
 
     # ---- e2e: the public host-buffer call, H2D bits + D2H amplitude inside the region ----
     e2e_steps = max(1, min(args.steps, 3))
     barrier()
     t0 = time.perf_counter()
-    for s in range(e2e_steps):
-        sl = s % n_slices
-        plan.contract(my_bits[0], sl, sl + 1)
+    for j in range(e2e_steps):
+        row, sl = step_args(j)
+        plan.contract(my_bits[row], sl, sl + step_slices)
     barrier()
     e2e_s = time.perf_counter() - t0
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t_e, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = flops_slice * e2e_steps * ws / float(t_e.item())
+    e2e_value = flops_step * e2e_steps * ws / float(t_e.item())
 
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return 0
     peaks, peak_src = load_peaks()
-    peak_tc = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / F16_FLOPS_PER_USEFUL
+    sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    if dtype == tb.TN_C64:
+        peak_tc = sustained / F16_FLOPS_PER_USEFUL
+        kname, pnote = "cgemm_f16x2s_kernel (tcgen05)", (
+            f"{peak_src} bf16 sustained {sustained} TF/s (= fp16 dense rate) x 8/24 (useful complex flops per "
+            "fp16 tensor flop of the fp16x2 scheme)")
+    else:
+        peak_tc = sustained * FP64_TC_PER_BF16
+        kname, pnote = "zgemm_dmma_kernel (FP64 tensor pipe, complex128)", (
+            f"{peak_src} bf16 sustained {sustained} TF/s x 40/2250 (B200 datasheet dense FP64-tensor / bf16 ratio); "
+            "complex128 flops are executed flops")
     gemm_tfs = prof["flops_gemm"] / (prof["ms_gemm"] / 1e3) / 1e12 if prof.get("ms_gemm") else 0.0
+    small_gbs = prof["bytes_small"] / (prof["ms_small"] / 1e3) / 1e9 if prof.get("ms_small") else 0.0
+    if prof.get("ms_gemm", 0) >= prof.get("ms_small", 0):
+        roof = {"bound": "tensor", "achieved": gemm_tfs, "peak": peak_tc, "unit": "TFLOP/s",
+                "frac": gemm_tfs / peak_tc if peak_tc else None, "traffic": None, "kernel": kname,
+                "peak_note": pnote, "share_of_step": prof["ms_gemm"] / ms if ms else None}
+    else:
+        roof = {"bound": "hbm", "achieved": small_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
+                "peak_note": f"{peak_src} HBM copy bandwidth; algorithmic bytes = operands + results of each wave",
+                "share_of_step": prof["ms_small"] / ms if ms else None}
+    if by_slices:
+        step_desc = (f"one slice (of 2^{slice_bits}) of one amplitude; rank r takes slices [rK, (r+1)K), "
+                     "partial amplitudes summed by one NCCL all-reduce in the timed region")
+    elif n_slices > 1:
+        step_desc = f"one slice (of {n_slices}) of one amplitude; rank r takes bitstrings r::N of {len(bits)}"
+    else:
+        step_desc = f"one full amplitude (unsliced); rank r takes bitstrings r::N of {len(bits)}"
+    prec = "block-scaled fp16x2 split on tcgen05" if dtype == tb.TN_C64 else "FP64 tensor pipe (DMMA)"
     line = {
         "metric": METRIC, "value": value, "unit": "FLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-        "config": {"workload": "configs[1]: 8x8 lattice, depth 16, Haar U(2) + CZ brickwork; complex64 "
-                               f"(block-scaled fp16x2 split on tcgen05); separator order seed 0; slicing to 2^{slice_log2}-entry tensors",
-                   "step": f"one slice (of {n_slices}) of one amplitude; rank r takes bitstrings r::N of 1024",
-                   "flops_per_step": flops_slice, "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice,
-                   "n_slices_per_amplitude": n_slices, "l2": "working set (GB intermediates) >> 126 MB L2, no flush",
+        "vs_baseline": None, "dtype": spec["dtype"], "data": "synthetic",
+        "config": {"workload": f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed "
+                               f"{ORDER_SEED}" + (f"; slicing to 2^{slice_log2}-entry tensors" if slice_log2 else ""),
+                   "step": step_desc, "flops_per_step": flops_step,
+                   "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice if flops_slice else None,
+                   "slice_bits": slice_bits,
+                   "l2": "working set (GB intermediates) >> 126 MB L2, no flush" if pinfo["arena_bytes"] > 1e9
+                         else "arena below L2 size: steps re-read warm intermediates (no flush)",
                    "arena_gb": pinfo["arena_bytes"] / 1e9},
         "amplitudes_per_s": amps_per_s,
-        "roofline": {"bound": "tensor", "achieved": gemm_tfs, "peak": peak_tc, "unit": "TFLOP/s",
-                     "frac": gemm_tfs / peak_tc if peak_tc else None, "traffic": None,
-                     "kernel": "cgemm_f16x2s_kernel (tcgen05)",
-                     "peak_note": f"{peak_src} bf16 sustained {peaks.get('bf16_tflops_sustained')} TF/s (= fp16 dense rate) "
-                                  "x 8/24 (useful complex flops per fp16 tensor flop of the fp16x2 scheme)",
-                     "share_of_step": prof["ms_gemm"] / ms if ms else None},
+        "roofline": roof,
         "kernel_ms": {k: prof[k] for k in ("ms_gemm", "ms_pack", "ms_small", "ms_other")},
-        "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(c.n),
-                "d2h_bytes_per_step": 8},
+        "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(nq),
+                "d2h_bytes_per_step": 16},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget, slice_log2=slice_log2)
+        line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget,
+                                                   slice_log2=slice_log2, hyper=spec["hyper"])
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
@@ -296,6 +359,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1, choices=sorted(SPEC))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()

@@ -47,7 +47,11 @@ enum {
 };
 
 enum { TN_C64 = 0, TN_C128 = 1 };               /* arithmetic type of a plan */
-enum { TN_PATH_AUTO = 0, TN_PATH_SMALL = 1, TN_PATH_TC = 2 };
+/* kernel path of a step: AUTO as a plan chooses; SMALL: warp-batched CUDA-core kernel;
+ * TC: tensor cores (tcgen05 fp16x2 for complex64, DMMA for complex128); SKINNY: CUDA-core
+ * split-K for few outputs and a long contraction; WIDE: CUDA-core tiles for a short
+ * contraction and a large output (the last two read planar packed operands). */
+enum { TN_PATH_AUTO = 0, TN_PATH_SMALL = 1, TN_PATH_TC = 2, TN_PATH_SKINNY = 3, TN_PATH_WIDE = 4 };
 
 typedef struct tn_network_s* tn_network;
 typedef struct tn_order_s* tn_order;
@@ -152,7 +156,7 @@ typedef struct {
 int tn_plan_get_info(tn_plan plan, tn_plan_info* info);
 
 /* tn_plan_steps: per step k (order of tn_order_steps), 6 int32 in out[6k..6k+5]:
- * path (TN_PATH_SMALL / TN_PATH_TC), log2 batch, log2 M, log2 N, log2 K (the GEMM
+ * path (TN_PATH_SMALL / TC / SKINNY / WIDE), log2 batch, log2 M, log2 N, log2 K (the GEMM
  * shape C[b][m][n] = sum_k A[b][m][k] B[b][k][n] as executed), launch position. */
 int tn_plan_steps(tn_plan plan, int32_t* out);
 
@@ -191,7 +195,8 @@ int tn_amplitudes(tn_plan plan, const uint8_t* bits, int32_t n_bits, double* amp
  * in C, and every index of C in A or B.  A, B, C: device buffers of `dtype`,
  * row-major over their index lists; dims[i] is the dimension of index id i
  * (0 <= i < n_dims, powers of two).  path: TN_PATH_AUTO picks the kernel like a
- * plan does; TN_PATH_SMALL / TN_PATH_TC force one (TN_PATH_TC requires complex64).
+ * plan does; TN_PATH_SMALL / TC / SKINNY / WIDE force one (TN_EUNSUPPORTED if the
+ * shape is outside what that kernel handles).
  * Asynchronous on `stream`; scratch memory is taken from an internal pool.
  */
 int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t* inds_a,

@@ -8,7 +8,9 @@ There is no Python or CPU fallback: if the library is missing, importing the
 binding's entry points raises.
 """
 from ._lib import (lib, TnError, Network, Order, Plan, OrderParams, contract_pair, kernel_launches,
-                   TN_C64, TN_C128, TN_PATH_AUTO, TN_PATH_SMALL, TN_PATH_TC, EXPORTED_SYMBOLS)
+                   TN_C64, TN_C128, TN_PATH_AUTO, TN_PATH_SMALL, TN_PATH_TC, TN_PATH_SKINNY, TN_PATH_WIDE,
+                   EXPORTED_SYMBOLS)
 
 __all__ = ["lib", "TnError", "Network", "Order", "Plan", "OrderParams", "contract_pair", "kernel_launches",
-           "TN_C64", "TN_C128", "TN_PATH_AUTO", "TN_PATH_SMALL", "TN_PATH_TC", "EXPORTED_SYMBOLS"]
+           "TN_C64", "TN_C128", "TN_PATH_AUTO", "TN_PATH_SMALL", "TN_PATH_TC", "TN_PATH_SKINNY",
+           "TN_PATH_WIDE", "EXPORTED_SYMBOLS"]

@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtn_b200.so")
 
 TN_C64, TN_C128 = 0, 1
-TN_PATH_AUTO, TN_PATH_SMALL, TN_PATH_TC = 0, 1, 2
+TN_PATH_AUTO, TN_PATH_SMALL, TN_PATH_TC, TN_PATH_SKINNY, TN_PATH_WIDE = 0, 1, 2, 3, 4
 
 EXPORTED_SYMBOLS = [
     "tn_last_error", "tn_version", "tn_build_network", "tn_network_free", "tn_network_get_info",

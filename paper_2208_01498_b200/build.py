@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SRCS = ["host/network.cpp", "host/order.cpp"]
 CUDA_SRCS = ["runtime.cu"]
-DEPS = ["host/tn_host.hpp", "device/common.cuh", "device/small.cu", "device/gemm_tc.cu", "device/zgemm.cu",
+DEPS = ["host/tn_host.hpp", "device/common.cuh", "device/small.cu", "device/gemm_tc.cu", "device/zgemm.cu", "device/skinny.cu",
         os.path.join("..", "..", "include", "tn.h")]
 
 

@@ -1,0 +1,217 @@
+// CUDA-core paths for the large steps that are not GEMM-shaped enough for the tensor
+// cores (Eq. (3), l.82-86: a step costs M = prod of all its index dimensions):
+//   * skinny: few outputs (M, N <= 64, M N <= 256 per batch) and a long contraction
+//     (K >= 2^10) -- HBM-bound on READING the operands once;
+//   * wide:   short contraction (K <= 16) and a large output -- HBM-bound on WRITING C.
+// Both read operands that the planar pack (pack_planar_kernel, the same smem-tiled
+// bit-permutation transpose as the tensor-core packs) has put in [b][re|im][rows][K]
+// layout, K contiguous, so every load is coalesced; accumulation is fp64.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace tnd {
+
+// ------------------------------------------------------------ planar pack ----
+// Output planes [b][2][rows][K] of R: (re plane, im plane); the host built tile_dst /
+// q_hi for 2 planes per batch (see PackDesc).
+template <typename R>
+__global__ void __launch_bounds__(PACK_THREADS) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+                                                                   const int64_t* __restrict__ tab,
+                                                                   R* __restrict__ out, int64_t src_base) {
+  using C2 = typename cplx_t<R>::type;
+  __shared__ __align__(16) C2 s[1 << PACK_MAX_T];
+  const C2* __restrict__ src = reinterpret_cast<const C2*>(ptrs[d.src]) + src_base;
+  const int64_t n_tiles = int64_t(1) << d.tile_bits;
+  const int64_t lmask = (int64_t(1) << d.ld) - 1;
+  const int T = 1 << d.t_bits;
+  int64_t so[PACK_PER_THREAD];
+  int sl[PACK_PER_THREAD];
+#pragma unroll
+  for (int i = 0; i < PACK_PER_THREAD; ++i) {
+    const int e = threadIdx.x + i * PACK_THREADS;
+    so[i] = e < T ? __ldg(tab + d.e_src + e) : 0;
+    sl[i] = e < T ? pack_slot((int)__ldg(tab + d.e_q + e)) : 0;
+  }
+  const int q0 = threadIdx.x * 8;
+  const bool writer = q0 < T;
+  const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t sb = gmap(tab, d.tile_src, tile);
+    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
+    C2 v[PACK_PER_THREAD];
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) v[i] = src[sb + so[i]];
+#pragma unroll
+    for (int i = 0; i < PACK_PER_THREAD; ++i)
+      if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
+    __syncthreads();
+    __align__(16) R re[8];
+    __align__(16) R im[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const C2 w = writer ? s[pack_slot(q0 + j)] : C2{0, 0};
+      re[j] = w.x;
+      im[j] = w.y;
+    }
+    __syncthreads();
+    if (!writer) continue;
+    // 8 consecutive elements per plane: two float4 / four double2 stores
+    constexpr int V = 16 / sizeof(R);
+    using V4 = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
+#pragma unroll
+    for (int j = 0; j < 8; j += V) {
+      *reinterpret_cast<V4*>(out + db + j) = *reinterpret_cast<const V4*>(&re[j]);
+      *reinterpret_cast<V4*>(out + db + d.plane + j) = *reinterpret_cast<const V4*>(&im[j]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- skinny ----
+// X [b][2][M][K], Y [b][2][N][K] (planar, K contiguous).  The M N outputs of a batch are
+// cut into groups of GM x GN <= 16 (GM = min(M, 4) rows of X, GN = min(N, 16 / GM) rows
+// of Y).  CTA (s, b) covers K range [s kc, (s + 1) kc); each of its 8 warps takes one
+// group (several warps per group interleave the range) and streams the group's rows
+// straight from HBM, lanes on consecutive k (coalesced 128-byte row segments, no shared
+// memory, no barriers), accumulating GM GN complex fp64 sums per lane.  Warp sums go to
+// partial[b][s * WS + w][o] (WS warps per group), summed in order by
+// skinny_reduce_kernel -- deterministic.
+constexpr int SK_THREADS = 256, SK_WARPS = SK_THREADS / 32;
+
+__host__ __device__ inline void skinny_groups(int m_bits, int n_bits, int& gm_bits, int& gn_bits, int& ng, int& ws) {
+  gm_bits = m_bits < 2 ? m_bits : 2;
+  gn_bits = n_bits < 4 - gm_bits ? n_bits : 4 - gm_bits;
+  ng = 1 << (m_bits - gm_bits + n_bits - gn_bits);
+  ws = ng >= SK_WARPS ? 1 : SK_WARPS / ng;
+}
+
+template <typename R, int GM, int GN>
+__global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict__ X, const R* __restrict__ Y,
+                                                            double2* __restrict__ partial, int32_t m_bits,
+                                                            int32_t n_bits, int64_t K, int64_t kc, int32_t S) {
+  int gm_bits, gn_bits, ng, ws;
+  skinny_groups(m_bits, n_bits, gm_bits, gn_bits, ng, ws);
+  const int M = 1 << m_bits, N = 1 << n_bits;
+  const int b = blockIdx.y, s = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k_begin = (int64_t)s * kc, k_end = min(K, k_begin + kc);
+  const R* __restrict__ xb = X + (int64_t)b * 2 * M * K;
+  const R* __restrict__ yb = Y + (int64_t)b * 2 * N * K;
+  for (int g = warp % ng; g < ng; g += SK_WARPS) {
+    const int wsub = (ng >= SK_WARPS) ? 0 : warp / ng;
+    const int m0 = (g >> (n_bits - gn_bits)) << gm_bits, n0 = (g & ((1 << (n_bits - gn_bits)) - 1)) << gn_bits;
+    double ar[GM][GN], ai[GM][GN];
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) { ar[i][j] = 0.0; ai[i][j] = 0.0; }
+    const R* xr_p = xb + (int64_t)m0 * K;
+    const R* xi_p = xb + (int64_t)(M + m0) * K;
+    const R* yr_p = yb + (int64_t)n0 * K;
+    const R* yi_p = yb + (int64_t)(N + n0) * K;
+    for (int64_t k = k_begin + wsub * 32 + lane; k < k_end; k += 32 * ws) {
+      double xr[GM], xi[GM], yr[GN], yi[GN];
+#pragma unroll
+      for (int i = 0; i < GM; ++i) { xr[i] = xr_p[(int64_t)i * K + k]; xi[i] = xi_p[(int64_t)i * K + k]; }
+#pragma unroll
+      for (int j = 0; j < GN; ++j) { yr[j] = yr_p[(int64_t)j * K + k]; yi[j] = yi_p[(int64_t)j * K + k]; }
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int j = 0; j < GN; ++j) {
+          ar[i][j] = fma(xr[i], yr[j], ar[i][j]);
+          ar[i][j] = fma(-xi[i], yi[j], ar[i][j]);
+          ai[i][j] = fma(xr[i], yi[j], ai[i][j]);
+          ai[i][j] = fma(xi[i], yr[j], ai[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) {
+        double re = ar[i][j], im = ai[i][j];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, off);
+          im += __shfl_xor_sync(0xffffffffu, im, off);
+        }
+        if (lane == 0)
+          partial[(((int64_t)b * S + s) * ws + wsub) * (M * N) + (m0 + i) * N + n0 + j] = make_double2(re, im);
+      }
+  }
+}
+
+// C[b][o] (+)= sum_s partial[b][s][o], in order
+template <typename R>
+__global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_t S, int32_t O, int64_t n_out,
+                                     void* const* __restrict__ ptrs, int32_t c_node, int32_t accumulate) {
+  using C2 = typename cplx_t<R>::type;
+  C2* C = reinterpret_cast<C2*>(ptrs[c_node]);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_out; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / O, o = i % O;
+    double re = 0.0, im = 0.0;
+    if (accumulate) { re = C[i].x; im = C[i].y; }
+    for (int s = 0; s < S; ++s) {
+      const double2 v = partial[(b * S + s) * O + o];
+      re += v.x;
+      im += v.y;
+    }
+    C[i] = C2{(R)re, (R)im};
+  }
+}
+
+// ------------------------------------------------------------------- wide ----
+// C[b][m][n] = sum_k X[b][m][k] Y[b][n][k] with K <= WD_MAXK (16): a CTA writes a tile of
+// WD_TM rows x WD_TN columns (consecutive threads on consecutive n: coalesced stores),
+// with the X rows and the Y columns of the tile staged in shared memory (Y transposed
+// to [k][n] so the per-thread reads are conflict-free).  Tiles are visited
+// grid-stride; batch b, row tile and column tile are flattened into one tile index.
+constexpr int WD_THREADS = 256, WD_TM = 32, WD_TN = 128, WD_MAXK = 16;
+
+template <typename R>
+__global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ X, const R* __restrict__ Y,
+                                                          void* const* __restrict__ ptrs, int32_t c_node,
+                                                          int32_t m_bits, int32_t n_bits, int32_t k_bits,
+                                                          int64_t n_tiles) {
+  using C2 = typename cplx_t<R>::type;
+  __shared__ double xs[2][WD_TM][WD_MAXK];       // fp64: each element converted once per tile
+  __shared__ double ys[2][WD_MAXK][WD_TN];
+  C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
+  const int64_t M = int64_t(1) << m_bits, N = int64_t(1) << n_bits;
+  const int K = 1 << k_bits;
+  const int tm = (int)(M < WD_TM ? M : WD_TM), tn = (int)(N < WD_TN ? N : WD_TN);
+  const int64_t mt = M / tm, nt = N / tn;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t b = tile / (mt * nt), r = tile % (mt * nt);
+    const int64_t m0 = (r / nt) * tm, n0 = (r % nt) * tn;
+    const R* __restrict__ xb = X + b * 2 * M * K;
+    const R* __restrict__ yb = Y + b * 2 * N * K;
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * tm * K; e += WD_THREADS) {
+      const int p = e / (tm * K), i = (e / K) % tm, k = e % K;
+      xs[p][i][k] = xb[(p * M + m0 + i) * K + k];
+    }
+    for (int e = threadIdx.x; e < 2 * tn * K; e += WD_THREADS) {
+      const int p = e / (tn * K), j = (e / K) % tn, k = e % K;
+      ys[p][k][j] = yb[(p * N + n0 + j) * K + k];
+    }
+    __syncthreads();
+    // threads: column j = tid % tn, row group rg = tid / tn (WD_THREADS / tn groups)
+    const int j = threadIdx.x % tn, groups = WD_THREADS / tn, rg = threadIdx.x / tn;
+    if (rg >= groups) continue;
+    for (int i = rg; i < tm; i += groups) {
+      double re = 0.0, im = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const double ar = xs[0][i][k], ai = xs[1][i][k], br = ys[0][k][j], bi = ys[1][k][j];
+        re = fma(ar, br, re);
+        re = fma(-ai, bi, re);
+        im = fma(ar, bi, im);
+        im = fma(ai, br, im);
+      }
+      C[(b * M + m0 + i) * N + n0 + j] = C2{(R)re, (R)im};
+    }
+  }
+}
+
+}  // namespace tnd

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -30,6 +31,7 @@
 #include "device/common.cuh"
 #include "device/gemm_tc.cu"
 #include "device/small.cu"
+#include "device/skinny.cu"
 #include "device/zgemm.cu"
 #include "host/tn_host.hpp"
 #include "tn.h"
@@ -189,8 +191,11 @@ void ensure_gemm_attr() {
 // one tensor-core step: pack X, pack Y, GEMM
 constexpr int KC_PER_SPLIT = 4096 / tnd::tc::BK;   // <= 4096 terms per TMEM accumulation
 
+enum { K_TC = 0, K_DMMA = 1, K_SKINNY = 2, K_WIDE = 3 };
 struct TcStep {
-  int kind = 0;                   // 0: complex64 block-scaled fp16x2 tcgen05; 1: complex128 DMMA
+  int kind = K_TC;                // K_TC: complex64 block-scaled fp16x2 tcgen05; K_DMMA: complex128
+                                  // DMMA; K_SKINNY / K_WIDE: CUDA-core split-K / wide (skinny.cu)
+  int esz = 8;                    // bytes per complex element of the plan
   PackDesc px, py;
   int64_t x_off = 0, y_off = 0;   // pack buffers (arena offsets)
   int64_t p_off = 0;              // split-K partials (arena offset), S > 1 only
@@ -208,13 +213,27 @@ struct TcStep {
 // 3 reduce, 4 other); time between consecutive marks is attributed to the earlier one
 struct Marks {
   std::vector<std::pair<cudaEvent_t, int>> v;
-  void mark(cudaStream_t st, int cat) {
+  std::vector<std::string> tags;
+  void mark(cudaStream_t st, int cat, std::string tag = "") {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     CK(cudaEventRecord(e, st));
     v.push_back({e, cat});
+    tags.push_back(std::move(tag));
   }
 };
+// TN_PROFILE_DUMP=<ms>: tn_contract_profiled prints every interval longer than <ms>
+double profile_dump_ms() {
+  static double v = [] {
+    const char* e = std::getenv("TN_PROFILE_DUMP");
+    return e ? std::atof(e) : -1.0;
+  }();
+  return v;
+}
+std::string shape_tag(const char* kind, int nb, int m, int n, int k) {
+  return std::string(kind) + " nb=" + std::to_string(nb) + " m=" + std::to_string(m) + " n=" + std::to_string(n) +
+         " k=" + std::to_string(k);
+}
 
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
 int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_bits + d.k_bits); }
@@ -244,9 +263,71 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
   CK(cudaGetLastError());
 }
 
+// partial sums per (batch, K split) of a skinny step: one per warp sharing an output group
+int skinny_ws(const TcStep& t) {
+  int gm, gn, ng, ws;
+  tnd::skinny_groups(t.m_bits, t.n_bits, gm, gn, ng, ws);
+  return ws;
+}
+
+// skinny / wide steps: planar packs + CUDA-core kernel (+ ordered split-K reduction)
+template <typename R>
+void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
+                      Marks* mk) {
+  auto pack = [&](const PackDesc& d, int64_t off, int64_t base) {
+    const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
+    tnd::pack_planar_kernel<R><<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
+        ptrs_d, d, tab_d, reinterpret_cast<R*>(arena + off), base);
+    g_launches++;
+  };
+  const R* X = reinterpret_cast<const R*>(arena + t.x_off);
+  const R* Y = reinterpret_cast<const R*>(arena + t.y_off);
+  const bool dump = profile_dump_ms() >= 0;
+  for (int s = 0; s < t.n_slabs; ++s) {
+    if (mk) mk->mark(st, 1, dump ? shape_tag("planar pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
+    pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
+    if (mk) mk->mark(st, 0, dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
+                                             t.k_bits) : "");
+    if (t.kind == K_SKINNY) {
+      const int64_t K = int64_t(1) << t.k_lo;
+      const int64_t kc = (K + t.S - 1) / t.S;
+      double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
+      int gm, gn, ng, ws;
+      tnd::skinny_groups(t.m_bits, t.n_bits, gm, gn, ng, ws);
+      const dim3 grid((unsigned)t.S, 1u << t.nb_bits);
+#define TN_SKINNY(GMB, GNB)                                                                                   \
+  if (gm == GMB && gn == GNB)                                                                                 \
+    tnd::skinny_kernel<R, 1 << GMB, 1 << GNB><<<grid, tnd::SK_THREADS, 0, st>>>(X, Y, partial, t.m_bits, t.n_bits, \
+                                                                                 K, kc, t.S);
+      TN_SKINNY(0, 0) TN_SKINNY(0, 1) TN_SKINNY(0, 2) TN_SKINNY(0, 3) TN_SKINNY(0, 4)
+      TN_SKINNY(1, 0) TN_SKINNY(1, 1) TN_SKINNY(1, 2) TN_SKINNY(1, 3)
+      TN_SKINNY(2, 0) TN_SKINNY(2, 1) TN_SKINNY(2, 2)
+#undef TN_SKINNY
+      g_launches++;
+      if (mk) mk->mark(st, 3);
+      const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 255) / 256, 148 * 16), 256, 0, st>>>(
+          partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      g_launches++;
+    } else {
+      const int64_t tm = std::min(tnd::WD_TM, 1 << t.m_bits), tn = std::min(tnd::WD_TN, 1 << t.n_bits);
+      const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits)) / (tm * tn);
+      tnd::wide_kernel<R><<<(unsigned)std::min<int64_t>(tiles, 148 * 8), tnd::WD_THREADS, 0, st>>>(
+          X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles);
+      g_launches++;
+    }
+  }
+  CK(cudaGetLastError());
+}
+
 void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                Marks* mk = nullptr) {
-  if (t.kind == 1) return launch_dmma(t, arena, ptrs_d, tab_d, st, mk);
+  if (t.kind == K_DMMA) return launch_dmma(t, arena, ptrs_d, tab_d, st, mk);
+  if (t.kind == K_SKINNY || t.kind == K_WIDE) {
+    if (t.esz == 8) return launch_cuda_core<float>(t, arena, ptrs_d, tab_d, st, mk);
+    return launch_cuda_core<double>(t, arena, ptrs_d, tab_d, st, mk);
+  }
   auto pack = [&](const PackDesc& d, int64_t off, int64_t base) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d.tile_bits, 148 * 8);
     tnd::pack_f16x2s_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
@@ -260,10 +341,10 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
   dim3 grid((unsigned)tiles, 1, (unsigned)((1u << t.nb_bits) * t.S));
   float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
   for (int s = 0; s < t.n_slabs; ++s) {
-    if (mk) mk->mark(st, 1);
+    if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
     pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
-    if (mk) mk->mark(st, 2);
+    if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     const int acc = s > 0;
     if (t.BN == 128) {
       ensure_gemm_attr<128>();
@@ -307,6 +388,8 @@ void finish_tc_shape(TcStep& t) {
   t.S = (int)((nk_all + KC_PER_SPLIT - 1) / KC_PER_SPLIT);
 }
 int64_t tc_partial_bytes(const TcStep& t) {
+  if (t.kind == K_SKINNY) return (int64_t(16) * t.S * skinny_ws(t)) << (t.nb_bits + t.m_bits + t.n_bits);
+  if (t.kind != K_TC) return 0;
   return t.S > 1 ? (int64_t(8) * t.S) << (t.nb_bits + t.m_bits + t.n_bits) : 0;
 }
 
@@ -431,12 +514,37 @@ bool want_tc(int dtype, int nb, int m, int n, int k) {
     return k >= 3 && std::max(m, n) >= 6 && std::min(m, n) >= 5 && (nb + m + n + k) >= 20;
   return k >= 4 && std::max(m, n) >= 6 && std::min(m, n) >= 4 && (nb + m + n + k) >= 22;
 }
+// CUDA-core paths for large non-GEMM-shaped steps (skinny.cu): long contraction with
+// few outputs, or short contraction with a large output
+bool want_skinny(int nb, int m, int n, int k) {
+  return k >= 10 && m <= 6 && n <= 6 && m + n <= 8 && nb <= 15 && (nb + m + n + k) >= 20;
+}
+bool want_wide(int nb, int m, int n, int k) {
+  return k <= 4 && (nb + m + n) >= 18 && nb <= 24 && (nb + m + k) >= 3 && (nb + n + k) >= 3;
+}
 void finish_tc_kind(TcStep& t, int dtype) {
-  t.kind = dtype == TN_C128 ? 1 : 0;
-  if (t.kind == 1) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; }
+  t.kind = dtype == TN_C128 ? K_DMMA : K_TC;
+  t.esz = dtype == TN_C128 ? 16 : 8;
+  if (t.kind == K_DMMA) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; }
+}
+// skinny / wide: K-slabs bound the planar pack buffers; skinny splits each slab's K
+// over S CTAs per batch (>= 4 waves of CTAs, >= 4096 K per CTA)
+void finish_cuda_core(TcStep& t, int dtype, int kind) {
+  t.kind = kind;
+  t.esz = dtype == TN_C128 ? 16 : 8;
+  t.BN = 0;
+  const int over = std::max(t.nb_bits + t.m_bits, t.nb_bits + t.n_bits) + t.k_bits - pack_cap_log2();
+  t.k_lo = kind == K_SKINNY ? std::max(std::min(t.k_bits, 6), t.k_bits - std::max(0, over)) : t.k_bits;
+  t.n_slabs = 1 << (t.k_bits - t.k_lo);
+  if (kind == K_SKINNY) {
+    const int64_t K = int64_t(1) << t.k_lo, want = std::max<int64_t>(1, (148 * 4) >> std::min(t.nb_bits, 20));
+    t.S = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 4096));
+  } else {
+    t.S = 1;
+  }
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
-  if (t.kind == 1) return int64_t(16) << (t.nb_bits + rows_bits + t.k_lo);
+  if (t.kind != K_TC) return int64_t(t.esz) << (t.nb_bits + rows_bits + t.k_lo);
   // 4 fp16 planes + one fp32 scale per row and 64-wide K chunk (+ slack: the GEMM's
   // scale copies read whole 128-row / BN-column tiles)
   return (int64_t(8) << (t.nb_bits + rows_bits + t.k_lo)) +
@@ -528,7 +636,9 @@ struct tn_plan_s {
         k += 1;
       } else {
         launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
-        k += tcs[L.second].kind ? 3 : tcs[L.second].n_slabs * (tcs[L.second].S > 1 ? 4 : 3);
+        const auto& t = tcs[L.second];
+        k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? 4 * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
+                                                                          : t.n_slabs * (t.S > 1 ? 4 : 3);
       }
     }
     if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
@@ -675,21 +785,31 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     Classes cl = classify(L[a], L[b], kept);
     int nb = sum_bits(cl.batch, l2), ml = sum_bits(cl.lfree, l2), mr = sum_bits(cl.rfree, l2), kk = sum_bits(cl.contr, l2);
     P.flops += 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
-    if (want_tc(P.dtype, nb, ml, mr, kk)) {
-      // X = operand with the larger free group becomes the MMA's M side
-      bool swap = mr > ml;
+    const int big = want_tc(P.dtype, nb, ml, mr, kk) ? (P.dtype == TN_C128 ? K_DMMA : K_TC)
+                    : want_skinny(nb, ml, mr, kk)  ? K_SKINNY
+                    : want_wide(nb, ml, mr, kk)    ? K_WIDE
+                                                   : -1;
+    if (big >= 0) {
+      // tensor cores: X = operand with the larger free group becomes the MMA's M side;
+      // wide: the larger free group becomes C's contiguous (column) side
+      bool swap = big == K_WIDE ? ml > mr : mr > ml;
       int X = swap ? b : a, Y = swap ? a : b;
       const auto& fx = swap ? cl.rfree : cl.lfree;
       const auto& fy = swap ? cl.lfree : cl.rfree;
       TcStep t;
       t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
-      finish_tc_shape(t);
       t.c_node = c;
-      finish_tc_kind(t, P.dtype);
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_y);
+      if (big == K_TC || big == K_DMMA) {
+        finish_tc_shape(t);
+        finish_tc_kind(t, P.dtype);
+      } else {
+        finish_cuda_core(t, P.dtype, big);
+      }
+      const int planes = t.kind == K_TC ? 4 : 2;
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, planes, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, planes, t.k_lo, &t.slab_y);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
-      P.tc_flops += t.flops;
+      if (t.kind == K_TC || t.kind == K_DMMA) P.tc_flops += t.flops;
       L[c].inds = cl.batch;
       L[c].inds.insert(L[c].inds.end(), fx.begin(), fx.end());
       L[c].inds.insert(L[c].inds.end(), fy.begin(), fy.end());
@@ -721,7 +841,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     int32_t* e = &P.step_table[6 * k];
     if (kind[k]) {
       const auto& t = P.tcs[big_index[k]];
-      e[0] = TN_PATH_TC; e[1] = t.nb_bits; e[2] = t.m_bits; e[3] = t.n_bits; e[4] = t.k_bits;
+      e[0] = t.kind == K_SKINNY ? TN_PATH_SKINNY : t.kind == K_WIDE ? TN_PATH_WIDE : TN_PATH_TC; e[1] = t.nb_bits; e[2] = t.m_bits; e[3] = t.n_bits; e[4] = t.k_bits;
     } else {
       const auto& d = small_desc[k];
       e[0] = TN_PATH_SMALL; e[1] = d.nb_bits; e[2] = d.m_bits; e[3] = d.n_bits; e[4] = d.k_bits;
@@ -804,7 +924,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     sizes.push_back(pack_bytes(t, t.n_bits));
     ivs.push_back({p0, p0 + 1});
     owner.push_back(-2 - 2 * big_index[k]);
-    if (t.S > 1) {
+    if (tc_partial_bytes(t) > 0) {
       sizes.push_back(tc_partial_bytes(t));
       ivs.push_back({p0 + 1, p0 + 1});
       owner.push_back(-1000000 - big_index[k]);
@@ -830,7 +950,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     }
   }
   for (auto& t : P.tcs) {
-    if (t.kind == 1) continue;
+    if (t.kind != K_TC) continue;
     t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 4);
     t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.BN, 4);
   }
@@ -888,7 +1008,17 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
     pr.n_other++;
     for (const auto& L : P.launches) {
       if (L.first == 0) {
-        mk.mark(st, 0);
+        {
+          const auto& w = P.waves[L.second];
+          size_t big = 0;
+          for (size_t q = 1; q < w.steps.size(); ++q) {
+            const auto &x = w.steps[q], &y = w.steps[big];
+            if (x.nb_bits + x.m_bits + x.n_bits + x.k_bits > y.nb_bits + y.m_bits + y.n_bits + y.k_bits) big = q;
+          }
+          const auto& d = w.steps[big];
+          mk.mark(st, 0, profile_dump_ms() >= 0 ? shape_tag(("wave of " + std::to_string(w.steps.size()) + ", largest").c_str(),
+                                                           d.nb_bits, d.m_bits, d.n_bits, d.k_bits) : "");
+        }
         if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
         else launch_wave<double>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
         pr.n_small++;
@@ -897,11 +1027,18 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
       } else {
         const auto& t = P.tcs[L.second];
         launch_tc(t, P.arena, P.ptrs_d, P.tab_d, st, &mk);
-        pr.n_gemm += t.kind ? 1 : t.n_slabs;
-        pr.n_pack += 2 * (t.kind ? 1 : t.n_slabs);
-        pr.flops_gemm += t.flops;
-        pr.bytes_pack += (t.kind ? 24.0 : 16.125) * (std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits) +
-                                                   std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits));
+        const double ex = std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits), ey = std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits);
+        pr.n_pack += 2 * t.n_slabs;
+        if (t.kind == K_SKINNY || t.kind == K_WIDE) {   // CUDA-core: accounted with the small path
+          pr.n_small += t.n_slabs;
+          pr.flops_small += t.flops;
+          pr.bytes_small += t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
+          pr.bytes_pack += 2.0 * t.esz * (ex + ey);
+        } else {
+          pr.n_gemm += t.n_slabs;
+          pr.flops_gemm += t.flops;
+          pr.bytes_pack += (t.kind == K_DMMA ? 32.0 : 16.125) * (ex + ey);
+        }
       }
     }
     mk.mark(st, 4);
@@ -914,6 +1051,8 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
     for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, mk.v[j].first, mk.v[j + 1].first));
+      if (profile_dump_ms() >= 0 && ms > profile_dump_ms())
+        fprintf(stderr, "[tn profile] %8.3f ms  cat %d  %s\n", ms, mk.v[j].second, mk.tags[j].c_str());
       switch (mk.v[j].second) {
         case 0: pr.ms_small += ms; break;
         case 1: pr.ms_pack += ms; break;
@@ -1207,8 +1346,21 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     const NodeLayout& LX = l_first ? LA : LB;
     const NodeLayout& LY = l_first ? LB : LA;
     int mx = sum_bits(g1, l2), my = sum_bits(g2, l2);
-    bool tc = path == TN_PATH_TC || (path == TN_PATH_AUTO && want_tc(dtype, nb, mx, my, kk));
-    if (tc && kk < (dtype == TN_C64 ? 4 : 1)) throw Err(TN_EUNSUPPORTED, "tensor-core path needs K >= 16 (complex64) / 2 (complex128)");
+    const int auto_kind = want_tc(dtype, nb, mx, my, kk) ? (dtype == TN_C128 ? K_DMMA : K_TC)
+                          : want_skinny(nb, mx, my, kk)   ? K_SKINNY
+                          : want_wide(nb, mx, my, kk)     ? K_WIDE
+                                                          : -1;
+    const int big = path == TN_PATH_TC       ? (dtype == TN_C128 ? K_DMMA : K_TC)
+                    : path == TN_PATH_SKINNY ? K_SKINNY
+                    : path == TN_PATH_WIDE   ? K_WIDE
+                    : path == TN_PATH_AUTO   ? auto_kind
+                                             : -1;
+    if (big == K_TC && kk < 4) throw Err(TN_EUNSUPPORTED, "tensor-core path needs K >= 16 (complex64)");
+    if (big == K_DMMA && kk < 1) throw Err(TN_EUNSUPPORTED, "DMMA path needs K >= 2 (complex128)");
+    if (big == K_SKINNY && (mx > 6 || my > 6 || mx + my > 8 || kk < 1 || nb > 15))
+      throw Err(TN_EUNSUPPORTED, "skinny path needs M, N <= 64, M N <= 256, K >= 2");
+    if (big == K_WIDE && (kk > 4 || nb + mx + kk < 3 || nb + my + kk < 3))
+      throw Err(TN_EUNSUPPORTED, "wide path needs K <= 16 and >= 8 entries per operand");
     cudaStream_t st = (cudaStream_t)stream;
     int cur = 0;
     CK(cudaGetDevice(&cur));
@@ -1229,14 +1381,19 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     };
     void** ptrs_d = (void**)dalloc(3 * sizeof(void*));
     h2d(ptrs_d, ptrs.data(), 3 * sizeof(void*));
-    if (tc) {
+    if (big >= 0) {
       TcStep t;
       t.nb_bits = nb; t.m_bits = mx; t.n_bits = my; t.k_bits = kk;
-      finish_tc_shape(t);
-      finish_tc_kind(t, dtype);
+      if (big == K_TC || big == K_DMMA) {
+        finish_tc_shape(t);
+        finish_tc_kind(t, dtype);
+      } else {
+        finish_cuda_core(t, dtype, big);
+      }
       t.c_node = 2;
-      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, t.kind ? 2 : 4, t.k_lo, &t.slab_y);
+      const int planes = t.kind == K_TC ? 4 : 2;
+      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, planes, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, planes, t.k_lo, &t.slab_y);
       size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
@@ -1245,7 +1402,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.x_off = 0;
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
-      if (t.kind == 0) {
+      if (t.kind == K_TC) {
         t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 4);
         t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.BN, 4);
       }

@@ -181,6 +181,63 @@ def test_pair_tensor_core_zero_chunks():
     assert np.all(np.abs(got - ref) <= c64_tol(2 ** 8) * bound + 1e-30)
 
 
+# CUDA-core paths for large non-GEMM-shaped steps (device/skinny.cu)
+SKINNY_CASES = [
+    (0, 3, 4, 12, None),      # 8 x 16 outputs, K = 4096
+    (0, 0, 0, 14, 3),         # full contraction to a scalar (one output), permuted
+    (2, 2, 3, 11, 4),         # batch 4, permuted layouts
+    (0, 6, 2, 10, 5),         # M = 64 rows, N = 4
+    (1, 3, 3, 5, None),       # K = 32: a single partial K tile
+]
+WIDE_CASES = [
+    (0, 7, 9, 3, None),       # 128 x 512 outputs, K = 8
+    (0, 5, 6, 0, 2),          # K = 1 (outer product), ragged tiles (M = 32 rows, N = 64), permuted
+    (3, 4, 8, 2, 6),          # batch 8, permuted
+    (0, 10, 4, 4, 7),         # N = 16 < tile width
+]
+
+
+@pytest.mark.parametrize("dtype", [tb.TN_C64, tb.TN_C128])
+@pytest.mark.parametrize("case", range(len(SKINNY_CASES)))
+def test_pair_skinny_path(case, dtype):
+    nb, m, n, k, ps = SKINNY_CASES[case]
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, dtype, tb.TN_PATH_SKINNY, seed=50 + case)
+    tol = 1e-12 if dtype == tb.TN_C128 else 4 * 2.0 ** -24      # fp64 accumulation, one rounding to fp32
+    assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
+
+
+@pytest.mark.parametrize("dtype", [tb.TN_C64, tb.TN_C128])
+@pytest.mark.parametrize("case", range(len(WIDE_CASES)))
+def test_pair_wide_path(case, dtype):
+    nb, m, n, k, ps = WIDE_CASES[case]
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    got, ref, bound = _run_pair(ia, ib, ic, dims, dtype, tb.TN_PATH_WIDE, seed=60 + case)
+    tol = 1e-12 if dtype == tb.TN_C128 else 4 * 2.0 ** -24
+    assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
+
+
+def test_pair_skinny_k_slabs():
+    """skinny path with K-slabs (pack cap lowered in a child process): the slab sums
+    accumulate into C."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        sys.path.insert(0, 'tests')
+        import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
+        for dt in (tb.TN_C64, tb.TN_C128):
+            ia, ib, ic, dims = T._gemm_case(1, 3, 2, 14, 8)
+            got, ref, bound = T._run_pair(ia, ib, ic, dims, dt, tb.TN_PATH_SKINNY, seed=33)
+            tol = 1e-12 if dt == tb.TN_C128 else 6 * 2.0 ** -24
+            assert np.all(np.abs(got - ref) <= tol * bound + 1e-30), (np.abs(got - ref) / bound).max()
+        print('ok')
+    """)
+    env = dict(os.environ, TN_PACK_CAP_LOG2="12")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 DMMA_CASES = [
     (0, 6, 6, 4, None),       # one 64x64 tile, K = 16
     (0, 5, 7, 3, 2),          # ragged M = 32, N = 128, K = 8, permuted
