@@ -218,6 +218,50 @@ __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t
                "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// cta_group::2 helpers: shared::cluster address of the same location in CTA rank 0 of the
+// cluster (the pair's leader), remote arrive, 2-SM TMA / MMA / commit
+__device__ __forceinline__ uint32_t mapa_rank0(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-SM TMA: data into this CTA's shared memory, completion bytes to the leader's barrier
+__device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* map, void* smem, uint32_t bar_cluster, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// arrive once on the barrier at this offset in both CTAs of the pair when the MMAs issued
+// so far complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 // K-major operand tile with 64-byte rows, SWIZZLE_64B: 8-row atoms of 512 B.
 __device__ __forceinline__ uint64_t make_desc_sw64(const void* smem) {
   const uint64_t addr = smem_u32(smem);
@@ -251,6 +295,136 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
+}
+
+// Epilogue warps of both GEMM kernels: promote every TMEM accumulation (one 64-wide
+// scale chunk) into fp32 registers, scaled by sA[row] * sB[col], then write C rows
+// [row0, row0 + 128) x columns [col0, col0 + BN) (C += when `acc_c`).  kPair: the
+// tempty barrier lives in the leader CTA of a cta_group::2 pair (remote arrive).
+template <int BN, bool kPair>
+__device__ __forceinline__ void epilogue(int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
+                                         uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int n_promo,
+                                         float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c) {
+  using CF = Cfg<BN>;
+  const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
+  const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  float ar[64], ai[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
+  for (int pi = 0; pi < n_promo; ++pi) {
+    const int buf = pi & 1, slot = pi % CF::SLOTS;
+    mbar_wait(&sfull[slot], (pi / CF::SLOTS) & 1);
+    mbar_wait(&tfull[buf], (pi >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t scs = smem_u32(sc + slot * (BM + BN));
+    const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
+    // column scales: one conflict-free load per lane, broadcast by shuffles (broadcast
+    // LDS.128s cost 4 shared wavefronts each, competing with the MMA operand reads)
+    const float sb_lo = lds_f32(scs + 4 * (BM + ch * 64 + lane));
+    const float sb_hi = lds_f32(scs + 4 * (BM + ch * 64 + 32 + lane));
+    const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;
+#pragma unroll
+    for (int c = 0; c < 64; c += 8) {
+      uint32_t vr[8], vi[8];
+      tmem_ld8(t_re + c, vr);
+      tmem_ld8(t_im + c, vi);
+      float sbl[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sbl[j] = __shfl_sync(0xffffffffu, (c + j) < 32 ? sb_lo : sb_hi, (c + j) & 31);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float s = sa * sbl[j];
+        ar[c + j] = __fmaf_rn(__uint_as_float(vr[j]), s, ar[c + j]);
+        ai[c + j] = __fmaf_rn(__uint_as_float(vi[j]), s, ai[c + j]);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncwarp();
+    if (lane == 0) {
+      if (kPair) mbar_arrive_cluster(mapa_rank0(&tempty[buf]));
+      else mbar_arrive(&tempty[buf]);
+      mbar_arrive(&sempty[slot]);
+    }
+  }
+  const int row = row0 + lg * 32 + lane;
+  const int col0 = col0_blk + ch * 64;
+  if (row < M && col0 < N) {
+    float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
+    if (acc_c) {        // K-slab > 0: C += this slab's product
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        ar[j] += (j < N - col0) ? crow[j].x : 0.f;
+        ai[j] += (j < N - col0) ? crow[j].y : 0.f;
+      }
+    }
+    if (N - col0 >= 64) {
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) *reinterpret_cast<float4*>(crow + j) = make_float4(ar[j], ai[j], ar[j + 1], ai[j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < N - col0) crow[j] = make_float2(ar[j], ai[j]);
+    }
+  }
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// MMA issue loop of the GEMM below (whole warp; one elected lane issues).  kTmem0: TMEM
+// base known to be 0.
+template <int BN, bool kTmem0>
+__device__ __forceinline__ void mma_loop(uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* tfull,
+                                         uint64_t* tempty, uint32_t tmem_rt, int nk) {
+  using CF = Cfg<BN>;
+  const uint32_t tmem = kTmem0 ? 0u : tmem_rt;
+  // idesc: F32 accumulate, F16 A/B, K-major both, N = BN, M = 128
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t idesc_negA = idesc | (1u << 13);
+  constexpr int PA[3] = {0, 0, 1};
+  constexpr int PB[3] = {0, 1, 0};
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc % CF::STAGES;
+    const uint32_t ph = (kc / CF::STAGES) & 1;
+    const int pi = kc / PROMO;
+    const int buf = pi & 1;
+    const bool first = (kc % PROMO) == 0;
+    const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
+    if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // epilogue drained this buffer
+    mbar_wait(&full[s], ph);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
+    uint8_t* st = smem + s * CF::STAGE;
+    if (elect_one()) {
+#pragma unroll
+    for (int ks = 0; ks < BK / 16; ++ks) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
+        const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
+        const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
+        const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
+        const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;   // fresh accumulator per promotion
+        mma_f16(t_re, a_re, b_re, idesc, acc);
+        mma_f16(t_re, a_im, b_im, idesc_negA, 1u);
+        mma_f16(t_im, a_re, b_im, idesc, acc);
+        mma_f16(t_im, a_im, b_re, idesc, 1u);
+      }
+    }
+    mma_commit(&empty[s]);                 // smem stage free once these MMAs have read it
+    if (last) mma_commit(&tfull[buf]);     // accumulator buffer ready for promotion
+    }
+    __syncwarp();
+  }
 }
 
 // Complex GEMM C[b][m][n] (+)= sum_k A[b][m][k] B[b][n][k] on block-scaled fp16x2
@@ -337,105 +511,182 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
       }
     }
   } else if (warp == MMA_WARP) {
-    if (lane == 0) {
-      // idesc: F32 accumulate, F16 A/B, K-major both, N = BN, M = 128
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-      const uint32_t idesc_negA = idesc | (1u << 13);
-      const int PA[3] = {0, 0, 1};
-      const int PB[3] = {0, 1, 0};
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % CF::STAGES;
-        const uint32_t ph = (kc / CF::STAGES) & 1;
-        const int pi = kc / PROMO;
-        const int buf = pi & 1;
-        const bool first = (kc % PROMO) == 0;
-        const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
-        if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // epilogue drained this buffer
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + BN;
-        uint8_t* st = smem + s * CF::STAGE;
-#pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
-            const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
-            const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
-            const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;   // fresh accumulator per promotion
-            mma_f16(t_re, a_re, b_re, idesc, acc);
-            mma_f16(t_re, a_im, b_im, idesc_negA, 1u);
-            mma_f16(t_im, a_re, b_im, idesc, acc);
-            mma_f16(t_im, a_im, b_re, idesc, 1u);
-          }
-        }
-        mma_commit(&empty[s]);      // smem stage free once these MMAs have read it
-        if (last) mma_commit(&tfull[buf]);    // accumulator buffer ready for promotion
-      }
-    }
+    // The whole warp runs the issue loop; one elected lane issues the MMAs and commits.
+    // With the whole TMEM allocated to this CTA its base is column 0: issuing with the
+    // literal base keeps every MMA operand in uniform registers (no per-MMA R2UR).
+    if (tmem == 0) mma_loop<BN, true>(smem, full, empty, tfull, tempty, 0u, nk);
+    else mma_loop<BN, false>(smem, full, empty, tfull, tempty, tmem, nk);
   } else {
     // ---- epilogue warps: promote every stage, scaled, into fp32 registers ----
-    const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
-    const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
-    const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
-    float ar[64], ai[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
-    for (int pi = 0; pi < n_promo; ++pi) {
-      const int buf = pi & 1, slot = pi % CF::SLOTS;
-      mbar_wait(&sfull[slot], (pi / CF::SLOTS) & 1);
-      mbar_wait(&tfull[buf], (pi >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t scs = smem_u32(sc + slot * (BM + BN));
-      const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
-      const uint32_t sbv = scs + 4 * (BM + ch * 64);
-      const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + BN;
-#pragma unroll
-      for (int c = 0; c < 64; c += 8) {
-        uint32_t vr[8], vi[8];
-        tmem_ld8(t_re + c, vr);
-        tmem_ld8(t_im + c, vi);
-        const float4 s0 = lds_f32x4(sbv + 4 * c), s1 = lds_f32x4(sbv + 4 * c + 16);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const float sbl[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float s = sa * sbl[j];
-          ar[c + j] = __fmaf_rn(__uint_as_float(vr[j]), s, ar[c + j]);
-          ai[c + j] = __fmaf_rn(__uint_as_float(vi[j]), s, ai[c + j]);
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) { mbar_arrive(&tempty[buf]); mbar_arrive(&sempty[slot]); }
-    }
-    // single split: write C; several: this split's fp32 partial (reduced in fp64 later)
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
-    const int row = m_blk * BM + lg * 32 + lane;
-    const int col0 = n_blk * BN + ch * 64;
-    if (row < M && col0 < N) {
-      float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
-      if (accumulate && !partial) {        // K-slab > 0: C += this slab's product
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          ar[j] += (j < N - col0) ? crow[j].x : 0.f;
-          ai[j] += (j < N - col0) ? crow[j].y : 0.f;
-        }
-      }
-      if (N - col0 >= 64) {
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) *reinterpret_cast<float4*>(crow + j) = make_float4(ar[j], ai[j], ar[j + 1], ai[j + 1]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < N - col0) crow[j] = make_float2(ar[j], ai[j]);
-      }
-    }
+    epilogue<BN, false>(warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, m_blk * BM,
+                        n_blk * BN, accumulate && !partial);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+}
+
+// ------------------------------------------------------- cta_group::2 GEMM ----
+// The same GEMM on CTA pairs (cluster of 2 on one TPC): the leader issues
+// tcgen05.mma.cta_group::2 with M = 256 (each CTA holds 128 rows of A) and N = 128 (each
+// CTA holds 64 rows of B, read by both tensor cores), so each SM streams 6 KB of
+// operands per 64-cycle MMA instead of 8 KB -- the single-CTA kernel is bound by the
+// shared-memory pipe (tensor reads + TMA writes), not the tensor core.  Both CTAs' TMA
+// loads complete on the leader's `full` barrier; the leader's commits arrive on `empty`
+// and `tfull` in both CTAs; both epilogues arrive on the leader's `tempty`.
+struct Cfg2 {
+  static constexpr int BN = 128, BNH = 64;
+  static constexpr int A_PLANE = BM * BK * 2, B_PLANE = BNH * BK * 2;
+  static constexpr int A_BYTES = 4 * A_PLANE, B_BYTES = 4 * B_PLANE;
+  static constexpr int STAGE = A_BYTES + B_BYTES;            // 48 KB per CTA
+  static constexpr int STAGES = 4;
+  static constexpr int SLOTS = Cfg<128>::SLOTS, SC_BYTES = Cfg<128>::SC_BYTES;
+  static constexpr int TMEM_COLS = Cfg<128>::TMEM_COLS, ACC_COLS = Cfg<128>::ACC_COLS;
+  static constexpr int EPI_WARPS = 8, THREADS = 32 * (EPI_WARPS + 2);
+  static constexpr int SMEM = STAGES * STAGE + SLOTS * SC_BYTES + 1024 + 512;
+};
+
+template <bool kTmem0>
+__device__ __forceinline__ void mma_loop_pair(uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* tfull,
+                                              uint64_t* tempty, uint32_t tmem_rt, int nk) {
+  using CF = Cfg2;
+  const uint32_t tmem = kTmem0 ? 0u : tmem_rt;
+  // idesc: F32 accumulate, F16 A/B, K-major both, N = 128, M = 256 (pair)
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(CF::BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  constexpr uint32_t idesc_negA = idesc | (1u << 13);
+  constexpr int PA[3] = {0, 0, 1};
+  constexpr int PB[3] = {0, 1, 0};
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc % CF::STAGES;
+    const uint32_t ph = (kc / CF::STAGES) & 1;
+    const int pi = kc / PROMO;
+    const int buf = pi & 1;
+    const bool first = (kc % PROMO) == 0;
+    const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
+    if (first) mbar_wait(&tempty[buf], ((pi >> 1) & 1) ^ 1);   // both epilogues drained this buffer
+    mbar_wait(&full[s], ph);                                     // both CTAs' halves landed
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + CF::BN;
+    uint8_t* st = smem + s * CF::STAGE;
+    if (elect_one()) {
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
+          const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
+          const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
+          const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
+          const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;
+          mma_f16_pair(t_re, a_re, b_re, idesc, acc);
+          mma_f16_pair(t_re, a_im, b_im, idesc_negA, 1u);
+          mma_f16_pair(t_im, a_re, b_im, idesc, acc);
+          mma_f16_pair(t_im, a_im, b_re, idesc, 1u);
+        }
+      }
+      mma_commit_pair(&empty[s]);                 // both CTAs' stage s free
+      if (last) mma_commit_pair(&tfull[buf]);     // both CTAs' accumulators ready
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
+    cgemm2_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const float* __restrict__ scA, const float* __restrict__ scB,
+                         void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
+                         int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate) {
+  using CF = Cfg2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* sc = reinterpret_cast<float*>(smem + CF::STAGES * CF::STAGE);   // [SLOTS][BM + BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE + CF::SLOTS * CF::SC_BYTES);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* tfull = empty + CF::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + CF::SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + CF::SLOTS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TMA_WARP = CF::EPI_WARPS, MMA_WARP = CF::EPI_WARPS + 1;
+  const uint32_t rank = cluster_ctarank();
+  // pair rasterization: groups of GROUP_M 256-row tiles sweep the N tiles together
+  const int n_tiles_m = (M + 255) / 256, n_tiles_n = N / CF::BN;
+  const int pid = blockIdx.x >> 1;
+  const int group = pid / (GROUP_M * n_tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gm = min(n_tiles_m - first_m, GROUP_M);
+  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
+  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+  const int row0 = m_blk * 256 + (int)rank * BM;
+  const int b = blockIdx.z % nb, split = blockIdx.z / nb;
+  const int nk_all = (K + BK - 1) / BK;
+  const int kc0 = split * kc_per_split;
+  const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+  const int nch_all = (nk_all + PROMO - 1) / PROMO;
+  const int n_promo = (nk + PROMO - 1) / PROMO;
+
+  if (warp == TMA_WARP && lane == 0) {
+    for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * CF::EPI_WARPS); }
+    for (int s = 0; s < CF::SLOTS; ++s) { mbar_init(&sfull[s], 1); mbar_init(&sempty[s], CF::EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();          // the peer's barriers are initialised before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == TMA_WARP) {
+    if (lane == 0) {
+      const float* sa = scA + ((int64_t)b * nch_all) * M + row0;
+      const float* sb = scB + ((int64_t)b * nch_all) * N + n_blk * CF::BN;
+      for (int kc = 0; kc < nk; ++kc) {
+        if (kc % PROMO == 0) {                  // this CTA's rows' and the tile's column scales
+          const int pi = kc / PROMO, slot = pi % CF::SLOTS, cg = (kc0 + kc) / PROMO;
+          mbar_wait(&sempty[slot], ((pi / CF::SLOTS) & 1) ^ 1);
+          mbar_expect_tx(&sfull[slot], CF::SC_BYTES);
+          float* d = sc + slot * (BM + CF::BN);
+          bulk_load(d, sa + (int64_t)cg * M, BM * 4, &sfull[slot]);
+          bulk_load(d + BM, sb + (int64_t)cg * N, CF::BN * 4, &sfull[slot]);
+        }
+        const int s = kc % CF::STAGES;
+        const uint32_t ph = (kc / CF::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * CF::STAGE);     // both CTAs' bytes
+        const uint32_t fb = mapa_rank0(&full[s]);
+        uint8_t* st = smem + s * CF::STAGE;
+        tma_load_3d_pair(&tmA, st, fb, (kc0 + kc) * BK, row0, b * 4);
+        tma_load_3d_pair(&tmB, st + CF::A_BYTES, fb, (kc0 + kc) * BK, n_blk * CF::BN + (int)rank * CF::BNH, b * 4);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    if (rank == 0) {
+      if (tmem == 0) mma_loop_pair<true>(smem, full, empty, tfull, tempty, 0u, nk);
+      else mma_loop_pair<false>(smem, full, empty, tfull, tempty, tmem, nk);
+    }
+  } else {
+    float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
+    epilogue<128, true>(warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
+                        n_blk * CF::BN, accumulate && !partial);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();          // no CTA leaves while its peer may still signal or read it
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+  }
 }
 
 }  // namespace tc

@@ -205,6 +205,7 @@ struct TcStep {
   std::vector<int64_t> slab_x, slab_y;   // source offsets of each slab
   int32_t c_node;
   int nb_bits, m_bits, n_bits, k_bits, BN;
+  bool pair = false;              // K_TC on CTA pairs (cta_group::2, 256 x 128 tiles)
   CUtensorMap ta, tb;
   double flops;
 };
@@ -346,7 +347,19 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
     pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
     if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     const int acc = s > 0;
-    if (t.BN == 128) {
+    if (t.pair) {
+      static bool attr2 = false;
+      if (!attr2) {
+        CK(cudaFuncSetAttribute(tnd::tc::cgemm2_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tnd::tc::Cfg2::SMEM));
+        attr2 = true;
+      }
+      const int64_t pairs = (int64_t(1) << (t.m_bits - 8)) * (int64_t(1) << (t.n_bits - 7));
+      dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
+      tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
+          KC_PER_SPLIT, partial, acc);
+    } else if (t.BN == 128) {
       ensure_gemm_attr<128>();
       tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
           t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
@@ -379,8 +392,18 @@ int pack_cap_log2() {
   return v;
 }
 
+// TN_GEMM_PAIR=0 disables the cta_group::2 GEMM (A/B comparisons)
+bool gemm_pair_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("TN_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 void finish_tc_shape(TcStep& t) {
   t.BN = (t.n_bits >= 7) ? 128 : 64;
+  t.pair = gemm_pair_enabled() && t.m_bits >= 8 && t.n_bits >= 7;
   const int over = std::max(t.nb_bits + t.m_bits, t.nb_bits + t.n_bits) + t.k_bits - pack_cap_log2();
   t.k_lo = std::max(std::min(t.k_bits, 5), t.k_bits - std::max(0, over));
   t.n_slabs = 1 << (t.k_bits - t.k_lo);
@@ -525,7 +548,7 @@ bool want_wide(int nb, int m, int n, int k) {
 void finish_tc_kind(TcStep& t, int dtype) {
   t.kind = dtype == TN_C128 ? K_DMMA : K_TC;
   t.esz = dtype == TN_C128 ? 16 : 8;
-  if (t.kind == K_DMMA) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; }
+  if (t.kind == K_DMMA) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; t.pair = false; }
 }
 // skinny / wide: K-slabs bound the planar pack buffers; skinny splits each slab's K
 // over S CTAs per batch (>= 4 waves of CTAs, >= 4096 K per CTA)
@@ -952,7 +975,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   for (auto& t : P.tcs) {
     if (t.kind != K_TC) continue;
     t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 4);
-    t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.BN, 4);
+    t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
   }
 
   // ---- uploads ----
@@ -1404,7 +1427,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
       if (t.kind == K_TC) {
         t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 4);
-        t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.BN, 4);
+        t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
       }
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies

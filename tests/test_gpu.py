@@ -115,6 +115,10 @@ TC_CASES = [
     (0, 10, 10, 12, 5),       # several tiles, K = 4096, permuted
     (0, 7, 8, 14, None),      # K = 16384: split-K over 4 CTAs + fp64 reduction
     (1, 6, 7, 13, 7),         # split-K with batch and ragged M
+    # M >= 256 and N >= 128: CTA-pair kernel (cta_group::2, 256 x 128 tiles)
+    (0, 8, 7, 4, None),       # one pair tile, K = 16
+    (2, 8, 7, 10, 3),         # batch 4, permuted, 32 stages
+    (0, 9, 9, 14, 11),        # 2 x 4 pair tiles, split-K over 4 splits, permuted
 ]
 
 
