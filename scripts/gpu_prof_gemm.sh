@@ -2,6 +2,6 @@
 set -x
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 python scripts/prof_gemm.py 13 13 12 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:cgemm -s 2 -c 1 -o gpurun_out/prof_cgemm python scripts/prof_gemm.py 13 13 12 > gpurun_out/ncu_cgemm.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:cgemm2 -s 2 -c 1 -o gpurun_out/prof_cgemm python scripts/prof_gemm.py 13 13 12 > gpurun_out/ncu_cgemm.log 2>&1
 echo ncu_rc=$?
 cat gpurun_out/prof_plain.log; tail -3 gpurun_out/ncu_cgemm.log
