@@ -79,7 +79,7 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 // [b][K / 64][r] fp32 (one per row and 64-element K chunk; one per row if K < 64).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
 // inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
-__global__ void __launch_bounds__(PACK_THREADS) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
                                                                    int64_t src_base) {
@@ -301,8 +301,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // scale chunk) into fp32 registers, scaled by sA[row] * sB[col], then write C rows
 // [row0, row0 + 128) x columns [col0, col0 + BN) (C += when `acc_c`).  kPair: the
 // tempty barrier lives in the leader CTA of a cta_group::2 pair (remote arrive).
+constexpr int EPI_PITCH = 132;   // floats per staged C row (64 complex + 16 B pad: conflict-free)
 template <int BN, bool kPair>
-__device__ __forceinline__ void epilogue(int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
+__device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
                                          uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int n_promo,
                                          float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c) {
   using CF = Cfg<BN>;
@@ -348,8 +349,31 @@ __device__ __forceinline__ void epilogue(int warp, int lane, uint32_t tmem, cons
       mbar_arrive(&sempty[slot]);
     }
   }
-  const int row = row0 + lg * 32 + lane;
   const int col0 = col0_blk + ch * 64;
+  if (col0 + 64 <= N) {
+    // Coalesced C: the warp's 32 x 64 complex block goes through shared memory (the
+    // operand stages: every MMA has completed, so they are free) and leaves one 512-byte
+    // row per instruction (thread-per-row stores would scatter 32 rows per instruction).
+    float* stg = stage_smem + warp * (32 * EPI_PITCH);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      *reinterpret_cast<float4*>(stg + lane * EPI_PITCH + 4 * j) = make_float4(ar[2 * j], ai[2 * j], ar[2 * j + 1], ai[2 * j + 1]);
+    __syncwarp();
+    const int rbase = row0 + lg * 32;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      if (rbase + r >= M) break;
+      float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_PITCH + 4 * lane);
+      float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * M + rbase + r) * (int64_t)N + col0) + lane;
+      if (acc_c) {
+        const float4 o = *dst;
+        v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+      }
+      *dst = v;
+    }
+    return;
+  }
+  const int row = row0 + lg * 32 + lane;
   if (row < M && col0 < N) {
     float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
     if (acc_c) {        // K-slab > 0: C += this slab's product
@@ -519,7 +543,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   } else {
     // ---- epilogue warps: promote every stage, scaled, into fp32 registers ----
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
-    epilogue<BN, false>(warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, m_blk * BM,
+    epilogue<BN, false>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, m_blk * BM,
                         n_blk * BN, accumulate && !partial);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -535,6 +559,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 // shared-memory pipe (tensor reads + TMA writes), not the tensor core.  Both CTAs' TMA
 // loads complete on the leader's `full` barrier; the leader's commits arrive on `empty`
 // and `tfull` in both CTAs; both epilogues arrive on the leader's `tempty`.
+static_assert(8 * 32 * 132 * 4 <= 3 * (4 * 128 * 32 * 2 + 4 * 128 * 32 * 2), "C staging must fit the operand stages");
 struct Cfg2 {
   static constexpr int BN = 128, BNH = 64;
   static constexpr int A_PLANE = BM * BK * 2, B_PLANE = BNH * BK * 2;
@@ -677,7 +702,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     }
   } else {
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
-    epilogue<128, true>(warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
+    epilogue<128, true>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
                         n_blk * CF::BN, accumulate && !partial);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

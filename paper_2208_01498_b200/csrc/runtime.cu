@@ -189,7 +189,9 @@ void ensure_gemm_attr() {
 }
 
 // one tensor-core step: pack X, pack Y, GEMM
-constexpr int KC_PER_SPLIT = 4096 / tnd::tc::BK;   // <= 4096 terms per TMEM accumulation
+// split-K only to fill the GPU: a step with few output tiles splits K over CTAs (each
+// split >= 16 stages), summed in fp64 by splitk_reduce_kernel
+constexpr int MIN_SPLIT_STAGES = 16;
 
 enum { K_TC = 0, K_DMMA = 1, K_SKINNY = 2, K_WIDE = 3 };
 struct TcStep {
@@ -206,6 +208,7 @@ struct TcStep {
   int32_t c_node;
   int nb_bits, m_bits, n_bits, k_bits, BN;
   bool pair = false;              // K_TC on CTA pairs (cta_group::2, 256 x 128 tiles)
+  int kc_split = 1 << 30;         // K stages per split (K_TC)
   CUtensorMap ta, tb;
   double flops;
 };
@@ -358,16 +361,16 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
       dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
       tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
           t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
-          KC_PER_SPLIT, partial, acc);
+          t.kc_split, partial, acc);
     } else if (t.BN == 128) {
       ensure_gemm_attr<128>();
       tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
           partial, acc);
     } else {
       ensure_gemm_attr<64>();
       tnd::tc::cgemm_f16x2s_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, KC_PER_SPLIT,
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
           partial, acc);
     }
     g_launches++;
@@ -408,7 +411,17 @@ void finish_tc_shape(TcStep& t) {
   t.k_lo = std::max(std::min(t.k_bits, 5), t.k_bits - std::max(0, over));
   t.n_slabs = 1 << (t.k_bits - t.k_lo);
   const int64_t nk_all = ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK;
-  t.S = (int)((nk_all + KC_PER_SPLIT - 1) / KC_PER_SPLIT);
+  // CTAs without split-K: 128 x BN tiles, or 256 x 128 tiles on CTA pairs (2 CTAs each)
+  const int64_t ctas = (int64_t(1) << t.nb_bits) *
+                       (t.pair ? 2 * (int64_t(1) << (t.m_bits - 8)) * (int64_t(1) << (t.n_bits - 7))
+                               : ((int64_t(1) << t.m_bits) + 127) / 128 * (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN));
+  const int64_t want = (2 * 148 + ctas - 1) / ctas;       // >= 2 waves
+  const int64_t smax = std::max<int64_t>(1, nk_all / MIN_SPLIT_STAGES);
+  t.S = (int)std::max<int64_t>(1, std::min(want, smax));
+  int64_t kc = (nk_all + t.S - 1) / t.S;
+  kc = (kc + tnd::tc::PROMO - 1) / tnd::tc::PROMO * tnd::tc::PROMO;   // splits start on a scale chunk
+  t.kc_split = (int)kc;
+  t.S = (int)((nk_all + kc - 1) / kc);
 }
 int64_t tc_partial_bytes(const TcStep& t) {
   if (t.kind == K_SKINNY) return (int64_t(16) * t.S * skinny_ws(t)) << (t.nb_bits + t.m_bits + t.n_bits);
@@ -529,6 +542,22 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   d.tile_dst = pool.add(gd);
   d.q_hi = pool.add(gq);
   return d;
+}
+
+// Order of the contracted indices in the packed K dimension.  With K-slabs the slab
+// bits are the HIGHEST K bits (the first indices of the list): take them from the
+// indices with the largest strides in the bigger operand, so every slab reads
+// contiguous runs of it (slab bits among its fast bits would read 1 element per
+// 2^bits, re-fetching each sector once per slab).
+std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& big, const std::vector<int>& l2,
+                              int n_slabs) {
+  std::vector<int> k = contr;
+  if (n_slabs <= 1) return k;
+  std::map<int, int> shift;   // bit position of each index in `big`
+  int sh = 0;
+  for (int j = (int)big.inds.size() - 1; j >= 0; --j) { shift[big.inds[j]] = sh; sh += l2[big.inds[j]]; }
+  std::stable_sort(k.begin(), k.end(), [&](int a, int b) { return shift.at(a) > shift.at(b); });
+  return k;
 }
 
 // decide the path of a step (TC only for complex64 GEMM-shaped steps)
@@ -829,8 +858,9 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
         finish_cuda_core(t, P.dtype, big);
       }
       const int planes = t.kind == K_TC ? 4 : 2;
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, cl.contr, l2, planes, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, cl.contr, l2, planes, t.k_lo, &t.slab_y);
+      const std::vector<int> kord = slab_k_order(cl.contr, L[X].bits >= L[Y].bits ? L[X] : L[Y], l2, t.n_slabs);
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, kord, l2, planes, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, Y, L[Y], cl.batch, fy, kord, l2, planes, t.k_lo, &t.slab_y);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       if (t.kind == K_TC || t.kind == K_DMMA) P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -1415,8 +1445,9 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       }
       t.c_node = 2;
       const int planes = t.kind == K_TC ? 4 : 2;
-      t.px = make_pack(pool, 0, LX, batch, g1, cl.contr, l2, planes, t.k_lo, &t.slab_x);
-      t.py = make_pack(pool, 1, LY, batch, g2, cl.contr, l2, planes, t.k_lo, &t.slab_y);
+      const std::vector<int> kord = slab_k_order(cl.contr, mx >= my ? LX : LY, l2, t.n_slabs);
+      t.px = make_pack(pool, 0, LX, batch, g1, kord, l2, planes, t.k_lo, &t.slab_x);
+      t.py = make_pack(pool, 1, LY, batch, g2, kord, l2, planes, t.k_lo, &t.slab_y);
       size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
