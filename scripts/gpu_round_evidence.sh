@@ -1,0 +1,10 @@
+# round evidence: all config bench lines + launch list of the default bench
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+for c in 3 2 4; do
+  timeout 1200 python bench.py --config $c --steps 3 --warmup 3 > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; echo rc=$?
+done
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo rc=$?
+python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bench_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+echo ncu_rc=$?
