@@ -161,10 +161,17 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=34, hyper=False):
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return {"value": flops / el, "unit": "FLOP/s", "cores": int(cores), "kind": "oracle",
+    return {"value": flops / el, "unit": "FLOP/s", "cores": int(cores), "kind": "oracle", "elapsed_s": el,
             "sample": f"oracle (numpy complex128) on slice 0 of bitstring 0: {done} of the {len(steps)} pairwise "
                       f"steps of the separator tree in order, skipping {skipped} steps with M > 2^33 or depending on "
                       f"one ({flops:.3g} flops, {el:.1f} s)"}
+
+
+def workload_name(ci, c, slice_log2):
+    spec = SPEC[ci]
+    prec = "block-scaled fp16x2 split on tcgen05" if spec["dtype"] == "c64" else "FP64 tensor pipe (DMMA)"
+    return (f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed {ORDER_SEED}"
+            + (f"; slicing to 2^{slice_log2}-entry tensors" if slice_log2 else ""))
 
 
 def run_reference(args):
@@ -179,10 +186,12 @@ def run_reference(args):
                                         slice_log2=spec["slice_logs"][0], hyper=spec["hyper"]))
     timed = vals[args.warmup:]
     v = float(np.mean([t["value"] for t in timed]))
+    cfg = {"workload": workload_name(args.config, c, spec["slice_logs"][0]),
+           "step": "a bounded sample of one slice's pairwise steps (see cpu_baseline.sample)"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "FLOP/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"configs[{args.config}] {c.name} (oracle, bounded sample per step)"},
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean([t["elapsed_s"] for t in timed])), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": "FLOP/s", "cores": timed[0]["cores"], "kind": "oracle",
                              "sample": timed[0]["sample"]},
             "e2e": {"value": v, "unit": "FLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -193,9 +202,14 @@ def run_reference(args):
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
-    if ws > 1:
+    # under torchrun (WORLD_SIZE set) the process group exists even for one rank, so the
+    # NCCL paths (barrier, slice all-reduce, max-over-ranks timing) run at every N
+    distributed = "WORLD_SIZE" in os.environ
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (no version banner)
+    if distributed:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2208_01498_b200 as tb
@@ -243,7 +257,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def barrier():
-        if ws > 1:
+        if distributed:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -260,14 +274,14 @@ def run_ours(args):
             p = plan.contract_profiled(bits_dev[row].data_ptr(), sl, sl + step_slices, amp.data_ptr(), sptr)
             for k, v in p.items():
                 prof[k] = prof.get(k, 0) + v
-        if by_slices and ws > 1:
+        if by_slices and distributed:
             torch.distributed.all_reduce(amp)        # partial amplitudes of all ranks' slices
         e1.record(stream)
         barrier()
     launches = tb.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if distributed:
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
     ms = float(t_max.item())
     flops_step = flops_slice * step_slices
@@ -285,12 +299,12 @@ def run_ours(args):
     barrier()
     e2e_s = time.perf_counter() - t0
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if distributed:
         torch.distributed.all_reduce(t_e, op=torch.distributed.ReduceOp.MAX)
     e2e_value = flops_step * e2e_steps * ws / float(t_e.item())
 
     if rank != 0:
-        if ws > 1:
+        if distributed:
             torch.distributed.destroy_process_group()
         return 0
     peaks, peak_src = load_peaks()
@@ -328,8 +342,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "FLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": spec["dtype"], "data": "synthetic",
-        "config": {"workload": f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed "
-                               f"{ORDER_SEED}" + (f"; slicing to 2^{slice_log2}-entry tensors" if slice_log2 else ""),
+        "config": {"workload": workload_name(ci, c, slice_log2),
                    "step": step_desc, "flops_per_step": flops_step,
                    "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice if flops_slice else None,
                    "slice_bits": slice_bits,
@@ -348,7 +361,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget,
                                                    slice_log2=slice_log2, hyper=spec["hyper"])
     print(json.dumps(line))
-    if ws > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
     return 0
 
