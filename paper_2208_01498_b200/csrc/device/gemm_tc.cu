@@ -299,13 +299,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // Epilogue warps of both GEMM kernels: promote every TMEM accumulation (one 64-wide
 // scale chunk) into fp32 registers, scaled by sA[row] * sB[col], then write C rows
-// [row0, row0 + 128) x columns [col0, col0 + BN) (C += when `acc_c`).  kPair: the
+// [row0, row0 + 128) x columns [col0, col0 + BN) (C += when `acc_c`); C is addressed as
+// [b][c_rows][N] with this launch's rows at c_row_off (row slabs of a larger C).  kPair: the
 // tempty barrier lives in the leader CTA of a cta_group::2 pair (remote arrive).
 constexpr int EPI_PITCH = 132;   // floats per staged C row (64 complex + 16 B pad: conflict-free)
 template <int BN, bool kPair>
 __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
                                          uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int n_promo,
-                                         float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c) {
+                                         float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c,
+                                         int c_rows, int c_row_off) {
   using CF = Cfg<BN>;
   const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
   const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
@@ -364,7 +366,7 @@ __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, 
     for (int r = 0; r < 32; ++r) {
       if (rbase + r >= M) break;
       float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_PITCH + 4 * lane);
-      float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * M + rbase + r) * (int64_t)N + col0) + lane;
+      float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * c_rows + c_row_off + rbase + r) * (int64_t)N + col0) + lane;
       if (acc_c) {
         const float4 o = *dst;
         v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
@@ -375,7 +377,7 @@ __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, 
   }
   const int row = row0 + lg * 32 + lane;
   if (row < M && col0 < N) {
-    float2* crow = C + ((int64_t)b * M + row) * (int64_t)N + col0;
+    float2* crow = C + ((int64_t)b * c_rows + c_row_off + row) * (int64_t)N + col0;
     if (acc_c) {        // K-slab > 0: C += this slab's product
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
@@ -463,7 +465,8 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const float* __restrict__ scA, const float* __restrict__ scB,
                         void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
-                        int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate) {
+                        int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate,
+                        int32_t m_off, int32_t M_c) {
   using CF = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     // ---- epilogue warps: promote every stage, scaled, into fp32 registers ----
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
     epilogue<BN, false>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, m_blk * BM,
-                        n_blk * BN, accumulate && !partial);
+                        n_blk * BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -621,7 +624,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     cgemm2_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const float* __restrict__ scA, const float* __restrict__ scB,
                          void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
-                         int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate) {
+                         int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate,
+                         int32_t m_off, int32_t M_c) {
   using CF = Cfg2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -703,7 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   } else {
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
     epilogue<128, true>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
-                        n_blk * CF::BN, accumulate && !partial);
+                        n_blk * CF::BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

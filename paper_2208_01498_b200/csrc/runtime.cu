@@ -209,6 +209,8 @@ struct TcStep {
   int nb_bits, m_bits, n_bits, k_bits, BN;
   bool pair = false;              // K_TC on CTA pairs (cta_group::2, 256 x 128 tiles)
   int kc_split = 1 << 30;         // K stages per split (K_TC)
+  int m_lo = 0;                   // log2 rows of X per row slab (= m_bits without row slabs)
+  int n_mslabs = 1;               // row slabs of X (bounded pack buffer when C is large)
   CUtensorMap ta, tb;
   double flops;
 };
@@ -341,15 +343,18 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
   };
   const float* sca = reinterpret_cast<const float*>(arena + t.x_off + plane_bytes(t.px));
   const float* scb = reinterpret_cast<const float*>(arena + t.y_off + plane_bytes(t.py));
-  const int64_t tiles = (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN) * (((int64_t(1) << t.m_bits) + 127) / 128);
+  const int64_t tiles = (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN) * (((int64_t(1) << t.m_lo) + 127) / 128);
   dim3 grid((unsigned)tiles, 1, (unsigned)((1u << t.nb_bits) * t.S));
   float2* partial = t.S > 1 ? reinterpret_cast<float2*>(arena + t.p_off) : nullptr;
+  // row slabs (outer) or K-slabs (inner); at most one of them has more than one slab
+  for (int ms = 0; ms < t.n_mslabs; ++ms)
   for (int s = 0; s < t.n_slabs; ++s) {
     if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
-    pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
-    pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
+    pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[t.n_mslabs > 1 ? ms : s]);
+    if (ms == 0) pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
     if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     const int acc = s > 0;
+    const int m_off = ms << t.m_lo;
     if (t.pair) {
       static bool attr2 = false;
       if (!attr2) {
@@ -357,21 +362,21 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
                                 tnd::tc::Cfg2::SMEM));
         attr2 = true;
       }
-      const int64_t pairs = (int64_t(1) << (t.m_bits - 8)) * (int64_t(1) << (t.n_bits - 7));
+      const int64_t pairs = (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7));
       dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
       tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
-          t.kc_split, partial, acc);
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
+          t.kc_split, partial, acc, m_off, 1 << t.m_bits);
     } else if (t.BN == 128) {
       ensure_gemm_attr<128>();
       tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
-          partial, acc);
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
+          partial, acc, m_off, 1 << t.m_bits);
     } else {
       ensure_gemm_attr<64>();
       tnd::tc::cgemm_f16x2s_kernel<64><<<grid, tnd::tc::Cfg<64>::THREADS, tnd::tc::Cfg<64>::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
-          partial, acc);
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.kc_split,
+          partial, acc, m_off, 1 << t.m_bits);
     }
     g_launches++;
     if (t.S > 1) {
@@ -406,19 +411,48 @@ bool gemm_pair_enabled() {
 
 void finish_tc_shape(TcStep& t) {
   t.BN = (t.n_bits >= 7) ? 128 : 64;
-  t.pair = gemm_pair_enabled() && t.m_bits >= 8 && t.n_bits >= 7;
-  const int over = std::max(t.nb_bits + t.m_bits, t.nb_bits + t.n_bits) + t.k_bits - pack_cap_log2();
-  t.k_lo = std::max(std::min(t.k_bits, 5), t.k_bits - std::max(0, over));
-  t.n_slabs = 1 << (t.k_bits - t.k_lo);
+  // Bounded pack buffers.  X (the larger operand) over the cap: row slabs of X when Y fits
+  // whole (each slab writes its own rows of C, no extra traffic), else K-slabs (C += per
+  // slab: 2|C| extra bytes per slab, cheap only when C is small).
+  const int cap = pack_cap_log2();
+  const int over_x = t.nb_bits + t.m_bits + t.k_bits - cap, over_y = t.nb_bits + t.n_bits + t.k_bits - cap;
+  t.m_lo = t.m_bits;
+  t.n_mslabs = 1;
+  t.k_lo = t.k_bits;
+  t.n_slabs = 1;
+  static const bool row_slabs = [] {
+    const char* e = std::getenv("TN_ROW_SLABS");
+    return !(e && e[0] == '0');
+  }();
+  if (row_slabs && over_x > 0 && over_y <= 0 && t.m_bits - over_x >= 8) {
+    t.m_lo = t.m_bits - over_x;
+    t.n_mslabs = 1 << over_x;
+  } else {
+    const int over = std::max(over_x, over_y);
+    t.k_lo = std::max(std::min(t.k_bits, 5), t.k_bits - std::max(0, over));
+    t.n_slabs = 1 << (t.k_bits - t.k_lo);
+  }
+  t.pair = gemm_pair_enabled() && t.m_lo >= 8 && t.n_bits >= 7;
   const int64_t nk_all = ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK;
   // CTAs without split-K: 128 x BN tiles, or 256 x 128 tiles on CTA pairs (2 CTAs each)
   const int64_t ctas = (int64_t(1) << t.nb_bits) *
-                       (t.pair ? 2 * (int64_t(1) << (t.m_bits - 8)) * (int64_t(1) << (t.n_bits - 7))
-                               : ((int64_t(1) << t.m_bits) + 127) / 128 * (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN));
-  const int64_t want = (2 * 148 + ctas - 1) / ctas;       // >= 2 waves
+                       (t.pair ? 2 * (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7))
+                               : ((int64_t(1) << t.m_lo) + 127) / 128 * (((int64_t(1) << t.n_bits) + t.BN - 1) / t.BN));
+  // split-K only below 2 waves; among the admissible splits take the best wave fill
+  // (units of residency: SMs, or SM pairs for the pair kernel)
   const int64_t smax = std::max<int64_t>(1, nk_all / MIN_SPLIT_STAGES);
-  t.S = (int)std::max<int64_t>(1, std::min(want, smax));
-  int64_t kc = (nk_all + t.S - 1) / t.S;
+  const int64_t unit = t.pair ? 2 : 1, slots = t.pair ? 74 : 148;
+  int64_t best = 1;
+  if (t.n_mslabs == 1 && ctas < 2 * 148) {
+    double best_eff = -1;
+    for (int64_t S = (2 * 148 + ctas - 1) / ctas; S <= std::min<int64_t>(smax, 8 * ((2 * 148 + ctas - 1) / ctas)); ++S) {
+      const double w = double(ctas / unit * S) / slots;
+      const double eff = w / std::ceil(w);
+      if (eff > best_eff + 0.02) { best_eff = eff; best = S; }
+    }
+    best = std::min<int64_t>(best, smax);
+  }
+  int64_t kc = (nk_all + best - 1) / best;
   kc = (kc + tnd::tc::PROMO - 1) / tnd::tc::PROMO * tnd::tc::PROMO;   // splits start on a scale chunk
   t.kc_split = (int)kc;
   t.S = (int)((nk_all + kc - 1) / kc);
@@ -459,15 +493,18 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
 // source offsets of the remaining high k bits, one per slab, are appended to `slabs`.
 PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
                    const std::vector<int>& rows, const std::vector<int>& kg, const std::vector<int>& l2,
-                   int planes = 6, int k_lo = -1, std::vector<int64_t>* slabs = nullptr) {
+                   int planes = 6, int k_lo = -1, std::vector<int64_t>* slabs = nullptr, int r_lo = -1) {
   PackDesc d{};
   d.src = src_node;
   d.nb_bits = sum_bits(batch, l2);
-  d.r_bits = sum_bits(rows, l2);
+  const int r_all = sum_bits(rows, l2);
   const int k_all = sum_bits(kg, l2);
   if (k_lo < 0 || k_lo > k_all) k_lo = k_all;
+  if (r_lo < 0 || r_lo > r_all) r_lo = r_all;
+  if (k_lo < k_all && r_lo < r_all) throw Err(TN_EINTERNAL, "pack: K-slabs and row slabs together");
   d.k_bits = k_lo;
-  const int D_all = d.nb_bits + d.r_bits + k_all;
+  d.r_bits = r_lo;
+  const int D_all = d.nb_bits + r_all + k_all;
   const int D = d.nb_bits + d.r_bits + d.k_bits, RK = d.r_bits + d.k_bits;
   d.plane = int64_t(1) << RK;
   // source bit of every destination bit
@@ -488,14 +525,17 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
       sh += l2[i];
     }
   }
-  // destination bits: k bits [0, k_lo) stay, [k_lo, k_all) are fixed per slab, the
-  // rest shift down by k_all - k_lo
-  for (int j = 0; j < D; ++j) pi[j] = j < k_lo ? pi_all[j] : pi_all[j + (k_all - k_lo)];
+  // destination bits of the full order: [0, k_all) K, [k_all, k_all + r_all) rows, then
+  // batch.  A slab fixes either the top K bits [k_lo, k_all) (K-slab) or the top row bits
+  // [k_all + r_lo, k_all + r_all) (row slab); the remaining bits shift down.
+  const int f0 = k_lo < k_all ? k_lo : k_all + r_lo;                 // first fixed bit
+  const int nf = (k_all - k_lo) + (r_all - r_lo);                   // fixed bits
+  for (int j = 0; j < D; ++j) pi[j] = j < f0 ? pi_all[j] : pi_all[j + nf];
   if (slabs) {
     slabs->clear();
-    for (int64_t s = 0; s < (int64_t(1) << (k_all - k_lo)); ++s) {
+    for (int64_t s = 0; s < (int64_t(1) << nf); ++s) {
       int64_t o = 0;
-      for (int u = 0; u < k_all - k_lo; ++u) if ((s >> u) & 1) o += int64_t(1) << pi_all[k_lo + u];
+      for (int u = 0; u < nf; ++u) if ((s >> u) & 1) o += int64_t(1) << pi_all[f0 + u];
       slabs->push_back(o);
     }
   }
@@ -544,11 +584,11 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   return d;
 }
 
-// Order of the contracted indices in the packed K dimension.  With K-slabs the slab
-// bits are the HIGHEST K bits (the first indices of the list): take them from the
-// indices with the largest strides in the bigger operand, so every slab reads
-// contiguous runs of it (slab bits among its fast bits would read 1 element per
-// 2^bits, re-fetching each sector once per slab).
+// Order of an index group (contracted K, or X's rows) in the packed operand.  With slabs
+// the slab bits are the HIGHEST bits of the group (its first indices): take them from
+// the indices with the largest strides in `big`, so every slab reads contiguous runs of
+// it (slab bits among its fast bits would read 1 element per 2^bits, re-fetching each
+// sector once per slab).
 std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& big, const std::vector<int>& l2,
                               int n_slabs) {
   std::vector<int> k = contr;
@@ -577,12 +617,17 @@ bool want_wide(int nb, int m, int n, int k) {
 void finish_tc_kind(TcStep& t, int dtype) {
   t.kind = dtype == TN_C128 ? K_DMMA : K_TC;
   t.esz = dtype == TN_C128 ? 16 : 8;
-  if (t.kind == K_DMMA) { t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; t.pair = false; }
+  if (t.kind == K_DMMA) {
+    t.S = 1; t.BN = tnd::zg::BN; t.k_lo = t.k_bits; t.n_slabs = 1; t.pair = false;
+    t.m_lo = t.m_bits; t.n_mslabs = 1;
+  }
 }
 // skinny / wide: K-slabs bound the planar pack buffers; skinny splits each slab's K
 // over S CTAs per batch (>= 4 waves of CTAs, >= 4096 K per CTA)
 void finish_cuda_core(TcStep& t, int dtype, int kind) {
   t.kind = kind;
+  t.m_lo = t.m_bits;
+  t.n_mslabs = 1;
   t.esz = dtype == TN_C128 ? 16 : 8;
   t.BN = 0;
   const int over = std::max(t.nb_bits + t.m_bits, t.nb_bits + t.n_bits) + t.k_bits - pack_cap_log2();
@@ -690,7 +735,7 @@ struct tn_plan_s {
         launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
         const auto& t = tcs[L.second];
         k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? 4 * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
-                                                                          : t.n_slabs * (t.S > 1 ? 4 : 3);
+             : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
     if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
@@ -846,7 +891,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       // wide: the larger free group becomes C's contiguous (column) side
       bool swap = big == K_WIDE ? ml > mr : mr > ml;
       int X = swap ? b : a, Y = swap ? a : b;
-      const auto& fx = swap ? cl.rfree : cl.lfree;
+      std::vector<int> fx = swap ? cl.rfree : cl.lfree;
       const auto& fy = swap ? cl.lfree : cl.rfree;
       TcStep t;
       t.nb_bits = nb; t.m_bits = sum_bits(fx, l2); t.n_bits = sum_bits(fy, l2); t.k_bits = kk;
@@ -859,7 +904,9 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       }
       const int planes = t.kind == K_TC ? 4 : 2;
       const std::vector<int> kord = slab_k_order(cl.contr, L[X].bits >= L[Y].bits ? L[X] : L[Y], l2, t.n_slabs);
-      t.px = make_pack(pool, X, L[X], cl.batch, fx, kord, l2, planes, t.k_lo, &t.slab_x);
+      // row slabs: X's largest-stride free indices first (the slab bits), in C's layout too
+      fx = slab_k_order(fx, L[X], l2, t.n_mslabs);
+      t.px = make_pack(pool, X, L[X], cl.batch, fx, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, Y, L[Y], cl.batch, fy, kord, l2, planes, t.k_lo, &t.slab_y);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       if (t.kind == K_TC || t.kind == K_DMMA) P.tc_flops += t.flops;
@@ -962,7 +1009,17 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     int c = n + (int)k;
     int born = 2 * step_pos[k] + 1;
     int hi = last;
-    if (parent[c] >= 0) hi = 2 * step_pos[parent[c]] + (kind[parent[c]] ? 0 : 1);
+    if (parent[c] >= 0) {
+      // a big step's operands die after its pack phase -- unless it packs in slabs: then
+      // slab s + 1 is packed after the GEMM of slab s wrote C, so they live through it
+      const int pk = parent[c];
+      bool slabbed = false;
+      if (kind[pk]) {
+        const auto& pt = P.tcs[big_index[pk]];
+        slabbed = pt.n_slabs > 1 || pt.n_mslabs > 1;
+      }
+      hi = 2 * step_pos[pk] + ((kind[pk] && !slabbed) ? 0 : 1);
+    }
     sizes.push_back((int64_t(1) << L[c].bits) * P.esz);
     ivs.push_back({born, hi});
     owner.push_back(c);
@@ -971,7 +1028,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     if (!kind[k]) continue;
     const auto& t = P.tcs[big_index[k]];
     const int p0 = 2 * step_pos[k];
-    sizes.push_back(pack_bytes(t, t.m_bits));
+    sizes.push_back(pack_bytes(t, t.m_lo));
     ivs.push_back({p0, p0 + 1});
     owner.push_back(-1 - 2 * big_index[k]);
     sizes.push_back(pack_bytes(t, t.n_bits));
@@ -1004,7 +1061,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   }
   for (auto& t : P.tcs) {
     if (t.kind != K_TC) continue;
-    t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_bits, t.nb_bits, 128, 4);
+    t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
     t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
   }
 
@@ -1088,7 +1145,8 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
           pr.bytes_small += t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
           pr.bytes_pack += 2.0 * t.esz * (ex + ey);
         } else {
-          pr.n_gemm += t.n_slabs;
+          pr.n_gemm += t.n_slabs * t.n_mslabs;
+          pr.n_pack += t.n_mslabs - 1;
           pr.flops_gemm += t.flops;
           pr.bytes_pack += (t.kind == K_DMMA ? 32.0 : 16.125) * (ex + ey);
         }
@@ -1446,9 +1504,9 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.c_node = 2;
       const int planes = t.kind == K_TC ? 4 : 2;
       const std::vector<int> kord = slab_k_order(cl.contr, mx >= my ? LX : LY, l2, t.n_slabs);
-      t.px = make_pack(pool, 0, LX, batch, g1, kord, l2, planes, t.k_lo, &t.slab_x);
+      t.px = make_pack(pool, 0, LX, batch, g1, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, 1, LY, batch, g2, kord, l2, planes, t.k_lo, &t.slab_y);
-      size_t xb = (size_t)pack_bytes(t, mx), yb = (size_t)pack_bytes(t, my);
+      size_t xb = (size_t)pack_bytes(t, t.kind == K_TC ? t.m_lo : mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);
       int64_t* tab_d = (int64_t*)dalloc(pool.v.size() * 8);
@@ -1457,7 +1515,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
       if (t.kind == K_TC) {
-        t.ta = make_plane_map(scratch + t.x_off, t.k_lo, mx, nb, 128, 4);
+        t.ta = make_plane_map(scratch + t.x_off, t.k_lo, t.m_lo, nb, 128, 4);
         t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
       }
       launch_tc(t, scratch, ptrs_d, tab_d, st);

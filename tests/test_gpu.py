@@ -266,7 +266,8 @@ def test_pair_tensor_core_k_slabs(monkeypatch):
         import sys; sys.path.insert(0, '.')
         sys.path.insert(0, 'tests')
         import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
-        for case in [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2)]:
+        # K-slabs, then row slabs of X (X over the cap, Y under it), with batch and permutations
+        for case in [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2), (0, 10, 7, 4, None), (1, 10, 7, 4, 3), (0, 11, 8, 4, 5)]:
             nb, m, n, k, ps = case
             ia, ib, ic, dims = T._gemm_case(nb, m, n, k, ps)
             got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=31)
@@ -275,6 +276,27 @@ def test_pair_tensor_core_k_slabs(monkeypatch):
         print('ok')
     """)
     env = dict(os.environ, TN_PACK_CAP_LOG2="13")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_plan_with_bounded_pack_buffers():
+    """A whole plan (6x6 lattice, tensor-core steps) with the pack cap lowered to 2^12 so
+    its GEMM steps run in K-slabs or row slabs; amplitudes against the oracle (child
+    process: the cap is read once per process)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        sys.path.insert(0, 'tests')
+        import test_gpu as T, paper_2208_01498_b200 as tb
+        from tn_inputs import lattice_cz
+        plan = T._plan_vs_oracle(lattice_cz(6, 6, 12, 8), tb.TN_C64, seed=0, n_bits=2)
+        st = plan.steps()
+        assert (st[:, 0] == tb.TN_PATH_TC).sum() >= 1
+        print('ok')
+    """)
+    env = dict(os.environ, TN_PACK_CAP_LOG2="12")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
