@@ -424,7 +424,12 @@ void finish_tc_shape(TcStep& t) {
     const char* e = std::getenv("TN_ROW_SLABS");
     return !(e && e[0] == '0');
   }();
-  if (row_slabs && over_x > 0 && over_y <= 0 && t.m_bits - over_x >= 8) {
+  // row slabs pay off only for a large C (K-slabs re-read and re-write it per slab) and
+  // keep >= 2 waves of CTAs per slab (no split-K inside row slabs)
+  const int m_slab = t.m_bits - std::max(over_x, 0);
+  const bool big_c = t.nb_bits + t.m_bits + t.n_bits >= 26;
+  const bool enough_tiles = t.nb_bits + m_slab + t.n_bits >= 14 + 9;   // >= 2^9 tiles of 128 x 128
+  if (row_slabs && over_x > 0 && over_y <= 0 && m_slab >= 8 && big_c && enough_tiles) {
     t.m_lo = t.m_bits - over_x;
     t.n_mslabs = 1 << over_x;
   } else {
