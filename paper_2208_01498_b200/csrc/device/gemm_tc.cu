@@ -718,6 +718,259 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   }
 }
 
+// ------------------------------------------------ persistent CTA-pair GEMM ----
+// cgemm2 as a persistent kernel: one CTA pair per TPC loops over the output tiles
+// (batch, split, 256 x 128 tile), so the TMA producer prefetches tile i + 1 while the
+// epilogue of tile i runs, and the MMA warp starts tile i + 1 in the TMEM buffer the
+// epilogue has released -- the per-CTA prologue/fill/drain of the one-tile-per-CTA
+// kernel (a third of the time of a K = 256 step) disappears.  All three roles walk the
+// same tile sequence with global stage / promotion counters.  C leaves through a
+// dedicated 20 KB staging area (8 complex per row per round, 64-byte row segments), the
+// operand stages being busy with the next tile.
+struct Cfg2P {
+  static constexpr int STG_PITCH = 20;                                 // floats per staged row (8 complex + pad)
+  static constexpr int STG_BYTES = Cfg2::EPI_WARPS * 32 * STG_PITCH * 4;
+  static constexpr int SMEM = Cfg2::STAGES * Cfg2::STAGE + Cfg2::SLOTS * Cfg2::SC_BYTES + STG_BYTES + 1024 + 512;
+};
+
+template <bool kTmem0>
+__device__ __forceinline__ void mma_tiles_pair(uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* tfull,
+                                               uint64_t* tempty, uint32_t tmem_rt, int pair, int n_pairs, int total,
+                                               int tiles_per_z, int nb, int nk_all, int kc_per_split) {
+  using CF = Cfg2;
+  const uint32_t tmem = kTmem0 ? 0u : tmem_rt;
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(CF::BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  constexpr uint32_t idesc_negA = idesc | (1u << 13);
+  constexpr int PA[3] = {0, 0, 1};
+  constexpr int PB[3] = {0, 1, 0};
+  int g = 0, gp = 0;                      // global stage / promotion counters
+  for (int tile = pair; tile < total; tile += n_pairs) {
+    const int split = (tile / tiles_per_z) / nb;
+    const int kc0 = split * kc_per_split;
+    const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+    for (int kc = 0; kc < nk; ++kc, ++g) {
+      const int s = g % CF::STAGES;
+      const uint32_t ph = (g / CF::STAGES) & 1;
+      const bool first = (kc % PROMO) == 0;
+      const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
+      const int buf = gp & 1;
+      if (first) mbar_wait(&tempty[buf], ((gp >> 1) & 1) ^ 1);
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t t_re = tmem + buf * CF::ACC_COLS, t_im = t_re + CF::BN;
+      uint8_t* st = smem + s * CF::STAGE;
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const uint64_t a_re = make_desc_sw64(st + (2 * PA[q] + 0) * CF::A_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t a_im = make_desc_sw64(st + (2 * PA[q] + 1) * CF::A_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t b_re = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 0) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint64_t b_im = make_desc_sw64(st + CF::A_BYTES + (2 * PB[q] + 1) * CF::B_PLANE) + (uint64_t)(ks * 2);
+            const uint32_t acc = (first && (ks | q) == 0) ? 0u : 1u;
+            mma_f16_pair(t_re, a_re, b_re, idesc, acc);
+            mma_f16_pair(t_re, a_im, b_im, idesc_negA, 1u);
+            mma_f16_pair(t_im, a_re, b_im, idesc, acc);
+            mma_f16_pair(t_im, a_im, b_re, idesc, 1u);
+          }
+        }
+        mma_commit_pair(&empty[s]);
+        if (last) mma_commit_pair(&tfull[buf]);
+      }
+      __syncwarp();
+      if (last) ++gp;
+    }
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
+    cgemm2p_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const float* __restrict__ scA, const float* __restrict__ scB,
+                          void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
+                          int32_t nb, int32_t S, int32_t kc_per_split, float2* __restrict__ partial,
+                          int32_t accumulate, int32_t m_off, int32_t M_c) {
+  using CF = Cfg2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* sc = reinterpret_cast<float*>(smem + CF::STAGES * CF::STAGE);   // [SLOTS][BM + BN]
+  float* stg = sc + CF::SLOTS * (BM + CF::BN);                          // [EPI_WARPS][32][STG_PITCH]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + Cfg2P::STG_BYTES);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* tfull = empty + CF::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + CF::SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + CF::SLOTS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TMA_WARP = CF::EPI_WARPS, MMA_WARP = CF::EPI_WARPS + 1;
+  const uint32_t rank = cluster_ctarank();
+  const int n_tiles_m = (M + 255) / 256, n_tiles_n = N / CF::BN;
+  const int tiles_per_z = n_tiles_m * n_tiles_n;
+  const int total = tiles_per_z * nb * S;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int nk_all = (K + BK - 1) / BK;
+  const int nch_all = (nk_all + PROMO - 1) / PROMO;
+  // tile -> (batch, split, m_blk, n_blk): groups of GROUP_M 256-row tiles sweep the N tiles
+  auto tile_coords = [&](int tile, int& b, int& split, int& m_blk, int& n_blk) {
+    const int z = tile / tiles_per_z, pid = tile % tiles_per_z;
+    b = z % nb;
+    split = z / nb;
+    const int group = pid / (GROUP_M * n_tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gm = min(n_tiles_m - first_m, GROUP_M);
+    m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
+    n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+  };
+
+  if (warp == TMA_WARP && lane == 0) {
+    for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * CF::EPI_WARPS); }
+    for (int s = 0; s < CF::SLOTS; ++s) { mbar_init(&sfull[s], 1); mbar_init(&sempty[s], CF::EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == TMA_WARP) {
+    if (lane == 0) {
+      int g = 0, gp = 0;
+      for (int tile = pair; tile < total; tile += n_pairs) {
+        int b, split, m_blk, n_blk;
+        tile_coords(tile, b, split, m_blk, n_blk);
+        const int row0 = m_blk * 256 + (int)rank * BM;
+        const int kc0 = split * kc_per_split;
+        const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+        const float* sa = scA + ((int64_t)b * nch_all) * M + row0;
+        const float* sb = scB + ((int64_t)b * nch_all) * N + n_blk * CF::BN;
+        for (int kc = 0; kc < nk; ++kc, ++g) {
+          if (kc % PROMO == 0) {
+            const int slot = gp % CF::SLOTS, cg = (kc0 + kc) / PROMO;
+            mbar_wait(&sempty[slot], ((gp / CF::SLOTS) & 1) ^ 1);
+            mbar_expect_tx(&sfull[slot], CF::SC_BYTES);
+            float* d = sc + slot * (BM + CF::BN);
+            bulk_load(d, sa + (int64_t)cg * M, BM * 4, &sfull[slot]);
+            bulk_load(d + BM, sb + (int64_t)cg * N, CF::BN * 4, &sfull[slot]);
+            ++gp;
+          }
+          const int s = g % CF::STAGES;
+          const uint32_t ph = (g / CF::STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * CF::STAGE);
+          const uint32_t fb = mapa_rank0(&full[s]);
+          uint8_t* st = smem + s * CF::STAGE;
+          tma_load_3d_pair(&tmA, st, fb, (kc0 + kc) * BK, row0, b * 4);
+          tma_load_3d_pair(&tmB, st + CF::A_BYTES, fb, (kc0 + kc) * BK, n_blk * CF::BN + (int)rank * CF::BNH, b * 4);
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    if (rank == 0) {
+      if (tmem == 0) mma_tiles_pair<true>(smem, full, empty, tfull, tempty, 0u, pair, n_pairs, total, tiles_per_z, nb, nk_all, kc_per_split);
+      else mma_tiles_pair<false>(smem, full, empty, tfull, tempty, tmem, pair, n_pairs, total, tiles_per_z, nb, nk_all, kc_per_split);
+    }
+  } else {
+    // ---- epilogue warps ----
+    const int lg = warp & 3, ch = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+    float* my_stg = stg + warp * (32 * Cfg2P::STG_PITCH);
+    int gp = 0;
+    for (int tile = pair; tile < total; tile += n_pairs) {
+      int b, split, m_blk, n_blk;
+      tile_coords(tile, b, split, m_blk, n_blk);
+      const int row0 = m_blk * 256 + (int)rank * BM;
+      const int kc0 = split * kc_per_split;
+      const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
+      const int n_promo = (nk + PROMO - 1) / PROMO;
+      float ar[64], ai[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
+      for (int p = 0; p < n_promo; ++p, ++gp) {
+        const int buf = gp & 1, slot = gp % CF::SLOTS;
+        mbar_wait(&sfull[slot], (gp / CF::SLOTS) & 1);
+        mbar_wait(&tfull[buf], (gp >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t scs = smem_u32(sc + slot * (BM + CF::BN));
+        const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
+        const float sb_lo = lds_f32(scs + 4 * (BM + ch * 64 + lane));
+        const float sb_hi = lds_f32(scs + 4 * (BM + ch * 64 + 32 + lane));
+        const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + CF::BN;
+#pragma unroll
+        for (int c = 0; c < 64; c += 8) {
+          uint32_t vr[8], vi[8];
+          tmem_ld8(t_re + c, vr);
+          tmem_ld8(t_im + c, vi);
+          float sbl[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sbl[j] = __shfl_sync(0xffffffffu, (c + j) < 32 ? sb_lo : sb_hi, (c + j) & 31);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float sv = sa * sbl[j];
+            ar[c + j] = __fmaf_rn(__uint_as_float(vr[j]), sv, ar[c + j]);
+            ai[c + j] = __fmaf_rn(__uint_as_float(vi[j]), sv, ai[c + j]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(mapa_rank0(&tempty[buf]));
+          mbar_arrive(&sempty[slot]);
+        }
+      }
+      // C tile rows [row0 + 32 lg, +32) x columns [n_blk 128 + 64 ch, +64): 8 rounds of
+      // 8 complex per row through the staging area, 4 lanes x 16 B per 64-byte row segment
+      float2* C;
+      int c_rows, c_row_off;
+      if (partial) { C = partial + (int64_t)split * nb * M * (int64_t)N; c_rows = M; c_row_off = 0; }
+      else { C = reinterpret_cast<float2*>(ptrs[c_node]); c_rows = M_c; c_row_off = m_off; }
+      const bool acc_c = accumulate && !partial;
+      const int rbase = row0 + lg * 32, col0 = n_blk * CF::BN + ch * 64;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<float4*>(my_stg + lane * Cfg2P::STG_PITCH + 4 * j) =
+              make_float4(ar[8 * q + 2 * j], ai[8 * q + 2 * j], ar[8 * q + 2 * j + 1], ai[8 * q + 2 * j + 1]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = i * 8 + (lane >> 2);
+          if (rbase + r < M) {
+            float4 v = *reinterpret_cast<const float4*>(my_stg + r * Cfg2P::STG_PITCH + 4 * (lane & 3));
+            float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * c_rows + c_row_off + rbase + r) * (int64_t)N +
+                                                    col0 + 8 * q) + (lane & 3);
+            if (acc_c) {
+              const float4 o = *dst;
+              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            *dst = v;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+  }
+}
+
 }  // namespace tc
 
 // C[i] = sum_s partial[s][i], summed in fp64 (split-K epilogue)

@@ -241,6 +241,15 @@ std::string shape_tag(const char* kind, int nb, int m, int n, int k) {
          " k=" + std::to_string(k);
 }
 
+// TN_GEMM_PERSIST=0 launches one CTA pair per output tile instead of the persistent kernel
+bool gemm_persist_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("TN_GEMM_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
 int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_bits + d.k_bits); }
 
@@ -355,7 +364,22 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
     if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     const int acc = s > 0;
     const int m_off = ms << t.m_lo;
-    if (t.pair) {
+    // persistent tile loop only for short K per tile (<= 32 stages): there the per-CTA
+    // prologue / fill / drain is a large share; long tiles are faster one per CTA pair
+    const int64_t stages_per_tile = std::min<int64_t>(t.kc_split, ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK);
+    if (t.pair && gemm_persist_enabled() && stages_per_tile <= 32) {
+      static bool attr2p = false;
+      if (!attr2p) {
+        CK(cudaFuncSetAttribute(tnd::tc::cgemm2p_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tnd::tc::Cfg2P::SMEM));
+        attr2p = true;
+      }
+      const int64_t tiles = (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7)) * (int64_t(1) << t.nb_bits) * t.S;
+      const int64_t n_pairs = std::min<int64_t>(tiles, 74);
+      tnd::tc::cgemm2p_f16x2s_kernel<<<(unsigned)(2 * n_pairs), tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2P::SMEM, st>>>(
+          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.S,
+          t.kc_split, partial, acc, m_off, 1 << t.m_bits);
+    } else if (t.pair) {
       static bool attr2 = false;
       if (!attr2) {
         CK(cudaFuncSetAttribute(tnd::tc::cgemm2_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
