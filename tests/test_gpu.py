@@ -481,3 +481,22 @@ def test_full_size_config_slices(ci, tgt):
         got = plan.contract(x, sid, sid + 1)
         scale = 2.0 ** (-c.n / 2 - nbits / 2)
         assert abs(got - want) <= 1e-5 * max(abs(want), scale), (sid, got, want)
+
+
+def test_config1_slices_with_bounded_pack_buffers():
+    """configs[1] at full size, slicing target 2^22, with the pack cap lowered to 2^18 so
+    its large steps run in K-slabs / row slabs (as the bench's 2^34 plan does at the
+    default cap): slices against oracle.contract_slice (child process: the cap is read
+    once per process)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        sys.path.insert(0, 'tests')
+        import test_gpu as T
+        T.test_full_size_config_slices(1, 22)
+        print('ok')
+    """)
+    env = dict(os.environ, TN_PACK_CAP_LOG2="18")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
