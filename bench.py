@@ -289,19 +289,41 @@ def run_ours(args):
     value = total_flops / (ms / 1e3)
     amps_per_s = value / (flops_slice * (2.0 ** slice_bits))
 
-    # ---- e2e: the public host-buffer call, H2D bits + D2H amplitude inside the region ----
+    # ---- e2e: the public host-buffer call, H2D bits (pinned host memory) + D2H amplitude
+    # inside the region ----
     e2e_steps = max(1, min(args.steps, 3))
+    pinned = torch.from_numpy(np.ascontiguousarray(my_bits)).pin_memory().numpy()
     barrier()
     t0 = time.perf_counter()
     for j in range(e2e_steps):
         row, sl = step_args(j)
-        plan.contract(my_bits[row], sl, sl + step_slices)
+        plan.contract(pinned[row], sl, sl + step_slices)
     barrier()
     e2e_s = time.perf_counter() - t0
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if distributed:
         torch.distributed.all_reduce(t_e, op=torch.distributed.ReduceOp.MAX)
     e2e_value = flops_step * e2e_steps * ws / float(t_e.item())
+
+    # ---- unsliced bitstring configs: throughput of tn_amplitudes with concurrent lanes ----
+    lanes_line = None
+    if not by_slices and n_slices == 1:
+        try:
+            plan.set_lanes(4)
+            batch = np.ascontiguousarray(my_bits[:64])
+            plan.amplitudes(batch[:8])
+            barrier()
+            t0 = time.perf_counter()
+            plan.amplitudes(batch)
+            barrier()
+            dt_l = time.perf_counter() - t0
+            t_l = torch.tensor([dt_l], dtype=torch.float64, device=dev)
+            if distributed:
+                torch.distributed.all_reduce(t_l, op=torch.distributed.ReduceOp.MAX)
+            lanes_line = {"lanes": 4, "amplitudes": int(len(batch)) * ws, "value": len(batch) * ws / float(t_l.item()),
+                          "unit": "amplitudes/s", "call": "tn_amplitudes (host bitstrings in, host amplitudes out)"}
+        except tb.TnError as e:
+            print(f"lanes: {e}", file=sys.stderr)
 
     if rank != 0:
         if distributed:
@@ -350,6 +372,7 @@ def run_ours(args):
                          else "arena below L2 size: steps re-read warm intermediates (no flush)",
                    "arena_gb": pinfo["arena_bytes"] / 1e9},
         "amplitudes_per_s": amps_per_s,
+        "amplitudes_per_s_lanes": lanes_line,
         "roofline": roof,
         "kernel_ms": {k: prof[k] for k in ("ms_gemm", "ms_pack", "ms_small", "ms_other")},
         "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(nq),

@@ -185,8 +185,16 @@ int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_be
                          void* amp_dev, void* stream, tn_profile* prof);
 /* tn_amplitudes: full amplitudes (all slices) of n_bits bitstrings
  * (host uint8[n_bits * n_qubits]) into host double[2 * n_bits]; host<->device
- * copies included.  Synchronizes `stream`. */
+ * copies included.  With lanes (tn_plan_set_lanes) bitstring j runs on lane j mod L,
+ * the lanes concurrently on their own streams (ordered after `stream`).  Synchronizes
+ * `stream`. */
 int tn_amplitudes(tn_plan plan, const uint8_t* bits, int32_t n_bits, double* amps, void* stream);
+/* tn_plan_set_lanes: give the plan n_lanes (>= 1) independent copies of its per-
+ * contraction device state (arena, pointer table, bitstring / slice / amplitude slots,
+ * tensor maps, stream, CUDA graph) so tn_amplitudes contracts n_lanes bitstrings at
+ * once; each lane costs one more arena (tn_plan_info.arena_bytes).  TN_ENOMEM (and the
+ * lanes made so far kept) when the next arena does not fit.  Lanes are never removed. */
+int tn_plan_set_lanes(tn_plan plan, int32_t n_lanes);
 
 /* ---------------------------------------------------------------- hot op ----
  * tn_contract_pair: C = sum over shared non-output indices of A * B (PAPER.md

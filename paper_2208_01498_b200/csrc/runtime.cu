@@ -749,31 +749,56 @@ struct tn_plan_s {
   cudaGraphExec_t graph = nullptr;
   int64_t kernels_per_slice = 0;
   std::vector<int32_t> step_table;   // 6 per step: path, nb, m, n, k, launch position
+  std::vector<int64_t> node_off;     // arena offset of every intermediate (-1: leaf)
 
-  void record(cudaStream_t st) {
+  // Extra lanes (tn_plan_set_lanes): independent copies of the per-contraction state --
+  // arena, pointer table, bitstring / slice / amplitude slots, tensor maps, stream and
+  // graph -- so tn_amplitudes runs several bitstrings concurrently.  Lane 0 is the
+  // plan's own state above.
+  struct Lane {
+    char* arena = nullptr;
+    void** ptrs_d = nullptr;
+    uint8_t* bits_d = nullptr;
+    int64_t* slice_d = nullptr;
+    double2* amp_d = nullptr;
+    std::vector<TcStep> tcs;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph = nullptr;
+  };
+  std::vector<Lane> extra;
+
+  void record(cudaStream_t st) { record_lane(st, arena, ptrs_d, bits_d, slice_d, amp_d, tcs); }
+  void record_lane(cudaStream_t st, char* arena_l, void** ptrs_l, uint8_t* bits_l, int64_t* slice_l, double2* amp_l,
+                   const std::vector<TcStep>& tcs_l) {
     tnd::set_leaf_ptrs_kernel<<<(n_leaves + 127) / 128, 128, 0, st>>>(
-        ptrs_d, leaf_base_d, var_begin_d, var_kind_d, var_stride_d, n_leaves, bits_d, slice_d, sl_log2_d, sl_shift_d,
+        ptrs_l, leaf_base_d, var_begin_d, var_kind_d, var_stride_d, n_leaves, bits_l, slice_l, sl_log2_d, sl_shift_d,
         esz, leaves);
     int64_t k = 1;
     for (auto& L : launches) {
       if (L.first == 0) {
-        if (dtype == TN_C64) launch_wave<float>(waves[L.second], ptrs_d, tab_d, st);
-        else launch_wave<double>(waves[L.second], ptrs_d, tab_d, st);
+        if (dtype == TN_C64) launch_wave<float>(waves[L.second], ptrs_l, tab_d, st);
+        else launch_wave<double>(waves[L.second], ptrs_l, tab_d, st);
         k += 1;
       } else {
-        launch_tc(tcs[L.second], arena, ptrs_d, tab_d, st);
-        const auto& t = tcs[L.second];
+        launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
+        const auto& t = tcs_l[L.second];
         k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? 4 * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
-    if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
-    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_d, root, root_exp, amp_d, slice_d);
+    if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_l, root, root_exp, amp_l, slice_l);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_l, root, root_exp, amp_l, slice_l);
     CK(cudaGetLastError());
     kernels_per_slice = k + 1;
   }
 
   ~tn_plan_s() {
+    for (auto& l : extra) {
+      if (l.graph) cudaGraphExecDestroy(l.graph);
+      if (l.stream) cudaStreamDestroy(l.stream);
+      for (void* p : {(void*)l.arena, (void*)l.ptrs_d, (void*)l.bits_d, (void*)l.slice_d, (void*)l.amp_d})
+        if (p) cudaFree(p);
+    }
     if (graph) cudaGraphExecDestroy(graph);
     if (cap) cudaStreamDestroy(cap);
     for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
@@ -1079,8 +1104,9 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
                              std::to_string(free_b));
   CK(cudaMalloc(&P.arena, P.arena_bytes));
   std::vector<void*> ptrs(P.n_nodes, nullptr);
+  P.node_off.assign(P.n_nodes, -1);
   for (size_t j = 0; j < owner.size(); ++j) {
-    if (owner[j] >= 0) ptrs[owner[j]] = P.arena + offs[j];
+    if (owner[j] >= 0) { ptrs[owner[j]] = P.arena + offs[j]; P.node_off[owner[j]] = offs[j]; }
     else if (owner[j] <= -1000000) P.tcs[-1000000 - owner[j]].p_off = offs[j];
     else {
       int o = -1 - owner[j];
@@ -1133,6 +1159,42 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   CK(cudaStreamEndCapture(P.cap, &g));
   CK(cudaGraphInstantiate(&P.graph, g, 0));
   CK(cudaGraphDestroy(g));
+}
+
+// one more lane of per-contraction state (see tn_plan_s::Lane)
+void add_lane(tn_plan_s& P) {
+  size_t free_b = 0, tot_b = 0;
+  CK(cudaMemGetInfo(&free_b, &tot_b));
+  if ((size_t)P.arena_bytes + (size_t(1) << 30) > free_b)
+    throw Err(TN_ENOMEM, "lane arena of " + std::to_string(P.arena_bytes) + " bytes does not fit free device memory");
+  tn_plan_s::Lane l;
+  CK(cudaMalloc(&l.arena, P.arena_bytes));
+  std::vector<void*> ptrs(P.n_nodes, nullptr);
+  for (int i = 0; i < P.n_nodes; ++i)
+    if (P.node_off[i] >= 0) ptrs[i] = l.arena + P.node_off[i];
+  l.ptrs_d = upload(ptrs);
+  CK(cudaMalloc(&l.bits_d, std::max(1, P.net->n_qubits)));
+  CK(cudaMemset(l.bits_d, 0, std::max(1, P.net->n_qubits)));
+  CK(cudaMalloc(&l.slice_d, sizeof(int64_t)));
+  CK(cudaMemset(l.slice_d, 0, sizeof(int64_t)));
+  CK(cudaMalloc(&l.amp_d, 16));
+  CK(cudaMemset(l.amp_d, 0, 16));
+  l.tcs = P.tcs;
+  for (auto& t : l.tcs) {
+    if (t.kind != K_TC) continue;
+    t.ta = make_plane_map(l.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
+    t.tb = make_plane_map(l.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
+  }
+  CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(l.stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = g_launches.load();
+  P.record_lane(l.stream, l.arena, l.ptrs_d, l.bits_d, l.slice_d, l.amp_d, l.tcs);
+  g_launches = before;
+  CK(cudaStreamEndCapture(l.stream, &g));
+  CK(cudaGraphInstantiate(&l.graph, g, 0));
+  CK(cudaGraphDestroy(g));
+  P.extra.push_back(std::move(l));
 }
 
 void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_profile& pr) {
@@ -1432,11 +1494,63 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
     if (!p || !amps || n_bits < 0 || (!bits && n_bits > 0)) throw Err(TN_EINVAL, "null");
     cudaStream_t st = (cudaStream_t)stream;
     const int nq = p->net->n_qubits;
-    for (int j = 0; j < n_bits; ++j) {
-      run_slices(*p, bits + (size_t)j * nq, false, 0, p->n_slices, st);
-      CK(cudaMemcpyAsync(amps + 2 * j, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+    CK(cudaSetDevice(p->device));
+    if (p->extra.empty() || n_bits < 2) {
+      for (int j = 0; j < n_bits; ++j) {
+        run_slices(*p, bits + (size_t)j * nq, false, 0, p->n_slices, st);
+        CK(cudaMemcpyAsync(amps + 2 * j, p->amp_d, 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      return;
     }
+    // lanes: bitstring j on lane j mod L, each lane on its own stream; bitstrings in, and
+    // amplitudes out, move in one copy each
+    const int L = 1 + (int)p->extra.size();
+    uint8_t* bits_all = nullptr;
+    double2* res = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&bits_all), std::max<size_t>(1, (size_t)n_bits * nq), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&res), (size_t)n_bits * 16, st));
+    if (nq > 0) CK(cudaMemcpyAsync(bits_all, bits, (size_t)n_bits * nq, cudaMemcpyHostToDevice, st));
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, st));
+    std::vector<cudaStream_t> ls(L);
+    ls[0] = p->cap;
+    for (int l = 1; l < L; ++l) ls[l] = p->extra[l - 1].stream;
+    for (int l = 0; l < L; ++l) CK(cudaStreamWaitEvent(ls[l], ready, 0));
+    for (int j = 0; j < n_bits; ++j) {
+      const int l = j % L;
+      cudaStream_t ss = ls[l];
+      uint8_t* bd = l ? p->extra[l - 1].bits_d : p->bits_d;
+      int64_t* sd = l ? p->extra[l - 1].slice_d : p->slice_d;
+      double2* ad = l ? p->extra[l - 1].amp_d : p->amp_d;
+      cudaGraphExec_t gr = l ? p->extra[l - 1].graph : p->graph;
+      if (nq > 0) CK(cudaMemcpyAsync(bd, bits_all + (size_t)j * nq, nq, cudaMemcpyDeviceToDevice, ss));
+      set_i64_kernel<<<1, 1, 0, ss>>>(sd, 0);
+      CK(cudaMemsetAsync(ad, 0, 16, ss));
+      for (int64_t s = 0; s < p->n_slices; ++s) {
+        CK(cudaGraphLaunch(gr, ss));
+        g_launches += p->kernels_per_slice;
+      }
+      CK(cudaMemcpyAsync(res + j, ad, 16, cudaMemcpyDeviceToDevice, ss));
+    }
+    for (int l = 0; l < L; ++l) {
+      CK(cudaEventRecord(ready, ls[l]));
+      CK(cudaStreamWaitEvent(st, ready, 0));
+    }
+    CK(cudaMemcpyAsync(amps, res, (size_t)n_bits * 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(bits_all, st));
+    CK(cudaFreeAsync(res, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventDestroy(ready));
+  });
+}
+
+int tn_plan_set_lanes(tn_plan p, int32_t n_lanes) {
+  return guard([&] {
+    if (!p || n_lanes < 1) throw Err(TN_EINVAL, "tn_plan_set_lanes: bad arguments");
+    CK(cudaSetDevice(p->device));
+    while ((int)p->extra.size() + 1 < n_lanes) add_lane(*p);
   });
 }
 

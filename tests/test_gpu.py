@@ -500,3 +500,25 @@ def test_config1_slices_with_bounded_pack_buffers():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_lanes_concurrent_amplitudes():
+    """tn_plan_set_lanes: configs[0] (complex128) and a 6x6 complex64 lattice with
+    tensor-core steps, 3 lanes, amplitudes of 7 bitstrings against the oracle (lane j mod 3
+    contracts bitstring j concurrently) and bit-identical to the single-lane plan."""
+    _cuda()
+    for circ, dtype in ((config_circuit(0), tb.TN_C128), (lattice_cz(6, 6, 12, 8), tb.TN_C64)):
+        on = build_network(circ)
+        osteps, _ = find_order(on, seed=0)
+        cn = tb.Network.from_circuit(circ)
+        co = tb.Order(cn, seed=0)
+        p1 = tb.Plan(cn, co, dtype=dtype)
+        bits = random_bitstrings(circ.n, 7, 5)
+        single = p1.amplitudes(bits)
+        p1.set_lanes(3)
+        multi = p1.amplitudes(bits)
+        assert np.array_equal(single, multi)
+        tol, scale = _amp_tol(dtype, circ.n)
+        for x, g in zip(bits, multi):
+            want = contract_tree(on, osteps, x)
+            assert abs(g - want) <= tol * max(abs(want), scale)
