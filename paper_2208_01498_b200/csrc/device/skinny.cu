@@ -16,7 +16,7 @@ namespace tnd {
 // Output planes [b][2][rows][K] of R: (re plane, im plane); the host built tile_dst /
 // q_hi for 2 planes per batch (see PackDesc).
 template <typename R>
-__global__ void __launch_bounds__(PACK_THREADS) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    R* __restrict__ out, int64_t src_base) {
   using C2 = typename cplx_t<R>::type;
@@ -142,22 +142,33 @@ __global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict_
   }
 }
 
-// C[b][o] (+)= sum_s partial[b][s][o], in order
+// C[b][o] (+)= sum_s partial[b][s][o]: one warp per output, lane l sums s = l, l + 32, ...
+// in order, then a fixed shuffle tree -- deterministic, and parallel when a long
+// contraction has few outputs (a scalar: S x 8 partials)
 template <typename R>
 __global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_t S, int32_t O, int64_t n_out,
                                      void* const* __restrict__ ptrs, int32_t c_node, int32_t accumulate) {
   using C2 = typename cplx_t<R>::type;
   C2* C = reinterpret_cast<C2*>(ptrs[c_node]);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_out; i += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_out; i += warps) {
     const int64_t b = i / O, o = i % O;
     double re = 0.0, im = 0.0;
-    if (accumulate) { re = C[i].x; im = C[i].y; }
-    for (int s = 0; s < S; ++s) {
+    for (int s = lane; s < S; s += 32) {
       const double2 v = partial[(b * S + s) * O + o];
       re += v.x;
       im += v.y;
     }
-    C[i] = C2{(R)re, (R)im};
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, off);
+      im += __shfl_xor_sync(0xffffffffu, im, off);
+    }
+    if (lane == 0) {
+      if (accumulate) { re += C[i].x; im += C[i].y; }
+      C[i] = C2{(R)re, (R)im};
+    }
   }
 }
 

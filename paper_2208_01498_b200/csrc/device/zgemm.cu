@@ -12,9 +12,9 @@
 namespace tnd {
 
 // ------------------------------------------------------------- fp64 pack -----
-// Same bit-permutation tiling as pack_bf16x3_kernel (see PackDesc); output planes
+// Same bit-permutation tiling as pack_f16x2s_kernel (see PackDesc); output planes
 // [b][2][rows][K] complex128 -> (re plane, im plane) of fp64.
-__global__ void __launch_bounds__(PACK_THREADS) pack_f64x2_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_f64x2_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                   const int64_t* __restrict__ tab,
                                                                   double* __restrict__ out, int64_t src_base) {
   __shared__ __align__(16) double2 s[1 << PACK_MAX_T];
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_f64x2_kernel(const void* co
   for (int i = 0; i < PACK_PER_THREAD; ++i) {
     const int e = threadIdx.x + i * PACK_THREADS;
     so[i] = e < T ? __ldg(tab + d.e_src + e) : 0;
-    sl[i] = e < T ? (int)__ldg(tab + d.e_q + e) : 0;
+    sl[i] = e < T ? pack_slot((int)__ldg(tab + d.e_q + e)) : 0;
   }
   const int q0 = threadIdx.x * 8;
   const bool writer = q0 < T;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_f64x2_kernel(const void* co
     double re[8], im[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double2 w = writer ? s[q0 + j] : double2{0.0, 0.0};
+      const double2 w = writer ? s[pack_slot(q0 + j)] : double2{0.0, 0.0};
       re[j] = w.x;
       im[j] = w.y;
     }

@@ -260,14 +260,14 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
     CK(cudaFuncSetAttribute(tnd::zg::zgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tnd::zg::SMEM));
     attr = true;
   }
-  if (mk) mk->mark(st, 1);
+  if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("f64 pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   for (const PackDesc* d : {&t.px, &t.py}) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d->tile_bits, 148 * 8);
     tnd::pack_f64x2_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
         ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)), 0);
     g_launches++;
   }
-  if (mk) mk->mark(st, 2);
+  if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("dmma", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
                         (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
@@ -322,7 +322,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       g_launches++;
       if (mk) mk->mark(st, 3);
       const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
-      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 255) / 256, 148 * 16), 256, 0, st>>>(
+      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
           partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
       g_launches++;
     } else {
