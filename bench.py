@@ -45,9 +45,10 @@ SPEC = {
     3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True),
     4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False),
 }
-# complex128 GEMM on DMMA: no measured fp64 peak on this pool -> measured bf16 sustained
-# x the B200 datasheet ratio of dense FP64 tensor (40 TF/s) to dense bf16 (2250 TF/s)
-FP64_TC_PER_BF16 = 40.0 / 2250.0
+# complex128 GEMM on DMMA: MEASURED_PEAKS.json has no fp64 figure; our own probe
+# (scripts/probes/dmma_peak.cu, profiles/r01/fp64_tensor_peak.md) measured 37.0 TF/s of
+# back-to-back register-only mma.sync f64 on this pool's B200 (burst clock)
+FP64_TC_TFLOPS = 37.0
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # split-precision complex64: one complex MAC (8 useful flops) = 4 real products x 3 fp16
 # piece products (hi.hi, hi.lo, lo.hi) = 24 fp16 tensor flops; fp16 dense rate = bf16 rate
@@ -337,10 +338,10 @@ def run_ours(args):
             f"{peak_src} bf16 sustained {sustained} TF/s (= fp16 dense rate) x 8/24 (useful complex flops per "
             "fp16 tensor flop of the fp16x2 scheme)")
     else:
-        peak_tc = sustained * FP64_TC_PER_BF16
+        peak_tc = FP64_TC_TFLOPS
         kname, pnote = "zgemm_dmma_kernel (FP64 tensor pipe, complex128)", (
-            f"{peak_src} bf16 sustained {sustained} TF/s x 40/2250 (B200 datasheet dense FP64-tensor / bf16 ratio); "
-            "complex128 flops are executed flops")
+            "fp64 tensor peak 37.0 TF/s measured by scripts/probes/dmma_peak.cu (register-only mma.sync f64, "
+            "burst clock; profiles/r01/fp64_tensor_peak.md); complex128 flops are executed flops")
     gemm_tfs = prof["flops_gemm"] / (prof["ms_gemm"] / 1e3) / 1e12 if prof.get("ms_gemm") else 0.0
     small_gbs = prof["bytes_small"] / (prof["ms_small"] / 1e3) / 1e9 if prof.get("ms_small") else 0.0
     if prof.get("ms_gemm", 0) >= prof.get("ms_small", 0):
