@@ -4,7 +4,7 @@
 // m16n8k4 f64 (SASS DMMA.8x8x4).  Operands come from the fp64 variant of the tiled
 // transpose pack: 2 planes (re, im) of [b][rows][K]; complex arithmetic is planar,
 // Cr += Ar.Br + (-Ai).Bi, Ci += Ar.Bi + Ai.Br, accumulated in fp64 registers.
-// CTA tile 64 x 64 complex, 4 warps of 32 x 32, K staged 16 at a time through a
+// CTA tile 64 x 64 complex, 8 warps of 32 x 16, K staged 16 at a time through a
 // 2-stage cp.async ring with an XOR swizzle of 16-byte chunks (conflict-free-ish
 // fragment loads).
 #include "common.cuh"
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f64x2_kernel(const void*
 
 // ------------------------------------------------------------------ DMMA -----
 namespace zg {
-constexpr int BM = 64, BN = 64, BK = 16, THREADS = 128, STAGES = 2;
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256, STAGES = 2;
 constexpr int PLANE_TILE = BM * BK;                       // doubles per plane per tile (BM == BN)
 constexpr int STAGE_DOUBLES = 4 * PLANE_TILE;             // A re, A im, B re, B im
 constexpr int SMEM = STAGES * STAGE_DOUBLES * 8;          // 64 KB
@@ -86,7 +86,7 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
 }
 
 // A planes: [b][2][M][K], B planes: [b][2][N][K] (fp64, K contiguous)
-__global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __restrict__ Ap, const double* __restrict__ Bp,
+__global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __restrict__ Ap, const double* __restrict__ Bp,
                                                              void* const* __restrict__ ptrs, int32_t c_node, int32_t M,
                                                              int32_t N, int32_t K) {
   extern __shared__ __align__(16) double sm[];
@@ -101,14 +101,14 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
   const double* A = Ap + (int64_t)b * 2 * M * (int64_t)K;
   const double* B = Bp + (int64_t)b * 2 * N * (int64_t)K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;   // 8 warps of 32 x 16
   const int g = lane >> 2, t = lane & 3;
 
   auto load_stage = [&](int stage, int k0) {
     double* st = sm + stage * STAGE_DOUBLES;
-    // 4 planes x 64 rows x 8 chunks of 16 B = 2048 chunks, 16 per thread
+    // 4 planes x 64 rows x 8 chunks of 16 B = 2048 chunks, 8 per thread
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 2048 / THREADS; ++i) {
       const int c = threadIdx.x + i * THREADS;
       const int plane = c >> 9;                  // 0: A re, 1: A im, 2: B re, 3: B im
       const int row = (c >> 3) & 63;
@@ -124,11 +124,11 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  double cr[2][4][4], ci[2][4][4];
+  double cr[2][2][4], ci[2][2][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) { cr[i][j][r] = 0.0; ci[i][j][r] = 0.0; }
 
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
     const double* sBi = st + 3 * PLANE_TILE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+      double ar[2][2], ai[2][2], nai[2][2], br[2], bi[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int r0 = wm + i * 16 + g;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
         nai[i][1] = -ai[i][1];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 2; ++j) {
         const int n0 = wn + j * 8 + g;
         br[j] = sBr[swz(n0, kk + t)];
         bi[j] = sBi[swz(n0, kk + t)];
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2; ++j) {
           dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
           dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
           dmma(ci[i][j], ar[i][0], ar[i][1], bi[j]);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(THREADS) zgemm_dmma_kernel(const double* __res
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int row = m_blk * BM + wm + i * 16 + g + 8 * h;
