@@ -89,7 +89,10 @@ __host__ __device__ inline void skinny_groups(int m_bits, int n_bits, int& gm_bi
 template <typename R, int GM, int GN>
 __global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict__ X, const R* __restrict__ Y,
                                                             double2* __restrict__ partial, int32_t m_bits,
-                                                            int32_t n_bits, int64_t K, int64_t kc, int32_t S) {
+                                                            int32_t n_bits, int64_t K, int64_t kc, int32_t S,
+                                                            void* const* __restrict__ ptrs, int32_t c_node,
+                                                            int32_t accumulate) {
+  using C2 = typename cplx_t<R>::type;
   int gm_bits, gn_bits, ng, ws;
   skinny_groups(m_bits, n_bits, gm_bits, gn_bits, ng, ws);
   const int M = 1 << m_bits, N = 1 << n_bits;
@@ -136,8 +139,15 @@ __global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict_
           re += __shfl_xor_sync(0xffffffffu, re, off);
           im += __shfl_xor_sync(0xffffffffu, im, off);
         }
-        if (lane == 0)
-          partial[(((int64_t)b * S + s) * ws + wsub) * (M * N) + (m0 + i) * N + n0 + j] = make_double2(re, im);
+        if (lane == 0) {
+          if (S * ws == 1) {        // one partial per output: write C directly
+            C2* C = reinterpret_cast<C2*>(ptrs[c_node]) + (int64_t)b * M * N + (m0 + i) * N + n0 + j;
+            if (accumulate) { re += C->x; im += C->y; }
+            *C = C2{(R)re, (R)im};
+          } else {
+            partial[(((int64_t)b * S + s) * ws + wsub) * (M * N) + (m0 + i) * N + n0 + j] = make_double2(re, im);
+          }
+        }
       }
   }
 }

@@ -314,12 +314,13 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
 #define TN_SKINNY(GMB, GNB)                                                                                   \
   if (gm == GMB && gn == GNB)                                                                                 \
     tnd::skinny_kernel<R, 1 << GMB, 1 << GNB><<<grid, tnd::SK_THREADS, 0, st>>>(X, Y, partial, t.m_bits, t.n_bits, \
-                                                                                 K, kc, t.S);
+                                                                                 K, kc, t.S, ptrs_d, t.c_node, s > 0);
       TN_SKINNY(0, 0) TN_SKINNY(0, 1) TN_SKINNY(0, 2) TN_SKINNY(0, 3) TN_SKINNY(0, 4)
       TN_SKINNY(1, 0) TN_SKINNY(1, 1) TN_SKINNY(1, 2) TN_SKINNY(1, 3)
       TN_SKINNY(2, 0) TN_SKINNY(2, 1) TN_SKINNY(2, 2)
 #undef TN_SKINNY
       g_launches++;
+      if (t.S * ws == 1) continue;      // the kernel wrote C
       if (mk) mk->mark(st, 3);
       const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
       tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
@@ -638,7 +639,9 @@ bool want_tc(int dtype, int nb, int m, int n, int k) {
 // CUDA-core paths for large non-GEMM-shaped steps (skinny.cu): long contraction with
 // few outputs, or short contraction with a large output
 bool want_skinny(int nb, int m, int n, int k) {
-  return k >= 10 && m <= 6 && n <= 6 && m + n <= 8 && nb <= 15 && (nb + m + n + k) >= 20;
+  // (K >= 64 with many batches: staging each batch's rows through L1 beats the small
+  // kernel's per-output re-reads of A and B)
+  return (k >= 10 || (k >= 6 && nb >= 6)) && m <= 6 && n <= 6 && m + n <= 8 && nb <= 15 && (nb + m + n + k) >= 20;
 }
 bool want_wide(int nb, int m, int n, int k) {
   return k <= 4 && (nb + m + n) >= 18 && nb <= 24 && (nb + m + k) >= 3 && (nb + n + k) >= 3;
@@ -782,7 +785,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? 4 * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
+        k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
