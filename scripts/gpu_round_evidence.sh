@@ -1,6 +1,8 @@
-# round evidence: all config bench lines + launch list of the default bench
+# round evidence: all tests, all config bench lines, launch list of the default bench
 set -x
 python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 1500 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 for c in 3 2 4; do
   timeout 1200 python bench.py --config $c --steps 3 --warmup 3 > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; echo rc=$?
 done
