@@ -79,7 +79,7 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 // [b][K / 64][r] fp32 (one per row and 64-element K chunk; one per row if K < 64).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
 // inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
-__global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 3) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
                                                                    int64_t src_base) {
@@ -102,17 +102,27 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void
   const int q0 = threadIdx.x * 8;                       // this thread's 8 destination elements
   const bool writer = q0 < T;                           // uniform per warp (T >= 256)
   const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t sb = gmap(tab, d.tile_src, tile);
-    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
-    float2 v[PACK_PER_THREAD];
+  // software pipeline: the next tile's loads are in flight while this tile goes through
+  // shared memory and out (twice the bytes in flight per thread)
+  float2 v[PACK_PER_THREAD];
+  if ((int64_t)blockIdx.x < n_tiles) {
+    const int64_t sb = gmap(tab, d.tile_src, blockIdx.x);
 #pragma unroll
     for (int i = 0; i < PACK_PER_THREAD; ++i)
       if (threadIdx.x + i * PACK_THREADS < T) v[i] = __ldg(src + sb + so[i]);
+  }
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
 #pragma unroll
     for (int i = 0; i < PACK_PER_THREAD; ++i)
       if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
     __syncthreads();
+    if (tile + gridDim.x < n_tiles) {
+      const int64_t sb = gmap(tab, d.tile_src, tile + gridDim.x);
+#pragma unroll
+      for (int i = 0; i < PACK_PER_THREAD; ++i)
+        if (threadIdx.x + i * PACK_THREADS < T) v[i] = __ldg(src + sb + so[i]);
+    }
     float4 w[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) w[j] = writer ? *reinterpret_cast<const float4*>(&s[pack_slot(q0 + 2 * j)]) : float4{};
