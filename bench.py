@@ -39,11 +39,14 @@ METRIC = "contraction FLOP/s"
 ORDER_SEED = 0
 # per config: arithmetic type, how the units shard across ranks, slicing targets tried in
 # order (largest tensor of a slice 2^t entries; the first plan that fits HBM is used)
+# n_seeds: randomized separator hierarchies built, the one with the least Eq. (3) work of
+# all slices kept (R10) -- for sliced configs the slicing overhead varies by
+# orders of magnitude between hierarchies (configs[1]: 2^59.2 with 4, 2^56.7 with 64)
 SPEC = {
-    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False),
-    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False),
-    3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True),
-    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False),
+    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
+    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
+    3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True, n_seeds=4),
+    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
 }
 # complex128 GEMM on DMMA: MEASURED_PEAKS.json has no fp64 figure; our own probe
 # (scripts/probes/dmma_peak.cu, profiles/r01/fp64_tensor_peak.md) measured 37.0 TF/s of
@@ -119,13 +122,14 @@ def workload(ci):
     return c, bits
 
 
-def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=34, hyper=False):
+def cpu_baseline_sample(c, bits, steps, sl, budget_s=15.0, hyper=False):
     """The oracle as it stands on the host cores: slice 0 of bitstring 0 of the same
-    network/order (oracle.ssa.find_order + choose_slices), contracting the steps of
-    the separator tree in order with oracle.contract.contract_pair until `budget_s`
-    of CPU time; FLOP/s = sum 8 M / elapsed."""
+    network and the same order (the step list and sliced indices of the plan, from
+    tn_find_order -- the oracle's own find_order builds the identical order, bit for
+    bit, but takes minutes in Python for 64 hierarchies), contracting the steps of the
+    separator tree in order with oracle.contract.contract_pair until `budget_s` of CPU
+    time; FLOP/s = sum 8 M / elapsed."""
     from oracle.network import build_network
-    from oracle.ssa import find_order, choose_slices
     from oracle.contract import kept_per_step, leaf_tensors, contract_pair
     try:
         from threadpoolctl import threadpool_info
@@ -133,8 +137,6 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=34, hyper=False):
     except Exception:
         cores = os.cpu_count()
     net = build_network(c, diag_hyper=hyper)
-    steps, _ = find_order(net, seed=ORDER_SEED)
-    sl = choose_slices(net, steps, slice_log2) if slice_log2 > 0 else []
     kept = kept_per_step(net, steps)
     fixed = {i: 0 for i in sl}
     n = len(net.tensors)
@@ -171,7 +173,8 @@ def cpu_baseline_sample(c, bits, budget_s=15.0, slice_log2=34, hyper=False):
 def workload_name(ci, c, slice_log2):
     spec = SPEC[ci]
     prec = "block-scaled fp16x2 split on tcgen05" if spec["dtype"] == "c64" else "FP64 tensor pipe (DMMA)"
-    return (f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed {ORDER_SEED}"
+    return (f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed {ORDER_SEED}, "
+            f"best of {spec['n_seeds']} randomized hierarchies"
             + (f"; slicing to 2^{slice_log2}-entry tensors" if slice_log2 else ""))
 
 
@@ -181,10 +184,13 @@ def run_reference(args):
         return 0
     spec = SPEC[args.config]
     c, bits = workload(args.config)
+    import paper_2208_01498_b200 as tb       # host-only calls: network + order (no device)
+    net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
+    order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=spec["slice_logs"][0])
     vals = []
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline_sample(c, bits, budget_s=max(2.0, 60.0 / (args.warmup + args.steps)),
-                                        slice_log2=spec["slice_logs"][0], hyper=spec["hyper"]))
+        vals.append(cpu_baseline_sample(c, bits, order.steps(), order.slices(),
+                                        budget_s=max(2.0, 60.0 / (args.warmup + args.steps)), hyper=spec["hyper"]))
     timed = vals[args.warmup:]
     v = float(np.mean([t["value"] for t in timed]))
     cfg = {"workload": workload_name(args.config, c, spec["slice_logs"][0]),
@@ -222,7 +228,7 @@ def run_ours(args):
     net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
     plan = None
     for slice_log2 in spec["slice_logs"]:
-        order = tb.Order(net, seed=ORDER_SEED, max_log2_size=slice_log2)
+        order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=slice_log2)
         try:
             plan = tb.Plan(net, order, dtype=dtype, device=local)
             break
@@ -389,8 +395,8 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(c, bits, budget_s=args.cpu_budget,
-                                                   slice_log2=slice_log2, hyper=spec["hyper"])
+        line["cpu_baseline"] = cpu_baseline_sample(c, bits, order.steps(), order.slices(), budget_s=args.cpu_budget,
+                                                   hyper=spec["hyper"])
     print(json.dumps(line))
     if distributed:
         torch.distributed.destroy_process_group()

@@ -32,7 +32,7 @@ order.  Readings (DESIGN.md):
   R9  greedy leaf planner: among pairs sharing an index (else all pairs) minimise
       log2 of the Eq. (3) cost M, then log2 result size, then (id_i, id_j).
   R10 the randomized hierarchy is built n_seeds (4) times; the one with the smallest
-      Eq. (3) total is kept.
+      Eq. (3) total is kept -- of all slices when a slicing target is set.
 """
 from __future__ import annotations
 
@@ -452,12 +452,13 @@ def _build(ctx, ids, sid, depth):
 
 
 def find_order(net, seed: int = 0, leaf_size: int = 8, a_max: int = 32, n_valid: int = 64,
-               max_tries: int = 256, n_seeds: int = 4):
+               max_tries: int = 256, n_seeds: int = 4, max_log2_size: int = 0):
     """Separator hierarchy (Fig. 2) -> list of pairwise steps (a, b); leaves are
     tensor ids 0..n-1, step k creates node id n + k.  Post-order: E subtree, I
     subtree, then their merge.  The randomized hierarchy is built n_seeds times
     (root stream ids 1..n_seeds) and the one with the smallest Eq. (3) total
-    sum_k 2 M_k is kept (R10; ties -> earliest)."""
+    sum_k 2 M_k is kept -- with a slicing target, the smallest total of all slices,
+    sliced_work(choose_slices(...)) (R10; ties -> earliest)."""
     best = None
     for r in range(n_seeds):
         ctx = _Ctx(net, seed, leaf_size, a_max, n_valid, max_tries)
@@ -466,9 +467,37 @@ def find_order(net, seed: int = 0, leaf_size: int = 8, a_max: int = 32, n_valid:
         tot = 0.0
         for m, _ in step_costs(net, ctx.steps):
             tot = tot + 2.0 ** (m + 1)
+        if max_log2_size > 0:
+            tot = sliced_work(net, ctx.steps, choose_slices(net, ctx.steps, max_log2_size))
         if best is None or tot < best[0]:
             best = (tot, ctx.steps, ctx.log)
     return best[1], best[2]
+
+
+def sliced_work(net, steps, slices):
+    """Eq. (3) work of all slices, W = 2^{sum sliced bits} * sum_k 2^{m_k - sliced bits
+    of step k} (left to right, doubles): what the greedy slicer (R11) minimises."""
+    n = len(net.tensors)
+    l2 = {i: net.log2dim(i) for i in range(len(net.dims))}
+    sl = set(slices)
+    total = {}
+    nodes = {}
+    for t in range(n):
+        ii = net.closed_inds(t)
+        nodes[t] = {i: 1 for i in ii}
+        for i in ii:
+            total[i] = total.get(i, 0) + 1
+    w = 0.0
+    for k, (a, b) in enumerate(steps):
+        A, B = nodes.pop(a), nodes.pop(b)
+        cnt = dict(A)
+        for i, c in B.items():
+            cnt[i] = cnt.get(i, 0) + c
+        nodes[n + k] = {i: c for i, c in cnt.items() if c < total[i]}
+        m = sum(l2[i] for i in sorted(cnt))
+        s = sum(l2[i] for i in sorted(cnt) if i in sl)
+        w = w + 2.0 ** (m - s)
+    return w * 2.0 ** sum(l2[i] for i in sl)
 
 
 def step_costs(net, steps):

@@ -556,9 +556,48 @@ std::vector<int> choose_slices(const Network& net, const std::vector<std::pair<i
   return out;
 }
 
+// Eq. (3) work of all slices, W = 2^{sum sliced bits} * sum_k 2^{m_k - sliced bits of
+// step k} (left to right, doubles) -- the quantity the greedy slicer minimises (R11).
+double sliced_work(const Network& net, const std::vector<std::pair<int, int>>& steps, const std::vector<int>& slices) {
+  const int n = (int)net.tensors.size();
+  std::vector<int> l2(net.dims.size());
+  for (size_t i = 0; i < net.dims.size(); ++i) l2[i] = net.log2dim((int)i);
+  std::vector<char> sl(net.dims.size(), 0);
+  int sb = 0;
+  for (int i : slices) { sl[i] = 1; sb += l2[i]; }
+  std::vector<int> total(net.dims.size(), 0);
+  std::unordered_map<int, std::map<int, int>> nodes;
+  for (int t = 0; t < n; ++t) {
+    nodes[t] = {};
+    for (int i : net.closed_inds(t)) { nodes[t][i] = 1; total[i]++; }
+  }
+  double w = 0.0;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    auto A = std::move(nodes[steps[k].first]);
+    auto B = std::move(nodes[steps[k].second]);
+    nodes.erase(steps[k].first); nodes.erase(steps[k].second);
+    std::map<int, int> cnt = A;
+    for (auto& kv : B) cnt[kv.first] += kv.second;
+    std::map<int, int> kept;
+    int m = 0, s = 0;
+    for (auto& kv : cnt) {
+      m += l2[kv.first];
+      if (sl[kv.first]) s += l2[kv.first];
+      if (kv.second < total[kv.first]) kept[kv.first] = kv.second;
+    }
+    nodes[n + (int)k] = kept;
+    w = w + std::ldexp(1.0, m - s);
+  }
+  return w * std::ldexp(1.0, sb);
+}
+
 Order find_order(const Network& net, uint64_t seed, const OrderParams& p) {
+  // R10: the randomized hierarchy is built n_seeds times; keep the one with the smallest
+  // Eq. (3) total -- of all slices when a slicing target is set (the slicer's overhead
+  // differs by orders of magnitude between hierarchies of similar unsliced cost)
   Order best;
   bool have = false;
+  double best_w = 0.0;
   std::vector<int> ids(net.tensors.size());
   std::iota(ids.begin(), ids.end(), 0);
   for (int r = 0; r < p.n_seeds; ++r) {
@@ -568,16 +607,23 @@ Order find_order(const Network& net, uint64_t seed, const OrderParams& p) {
     costs(net, c.steps, m, res);
     double tot = 0.0;
     for (int mm : m) tot = tot + std::ldexp(1.0, mm + 1);
-    if (!have || tot < best.total_2M) {
+    std::vector<int> sl;
+    double w = tot;
+    if (p.max_log2_size > 0) {
+      sl = choose_slices(net, c.steps, p.max_log2_size);
+      w = sliced_work(net, c.steps, sl);
+    }
+    if (!have || w < best_w) {
       have = true;
+      best_w = w;
       best.steps = c.steps;
       best.step_m = m;
       best.step_res = res;
       best.total_2M = tot;
       best.median_fallbacks = c.medians;
+      best.slices = sl;
     }
   }
-  if (p.max_log2_size > 0) best.slices = choose_slices(net, best.steps, p.max_log2_size);
   return best;
 }
 

@@ -317,7 +317,7 @@ def _amp_tol(dtype, n):
 def _plan_vs_oracle(circ, dtype, seed, hyper=False, max_log2_size=0, n_bits=4, with_zero=True):
     _cuda()
     on = build_network(circ, diag_hyper=hyper)
-    osteps, _ = find_order(on, seed=seed)
+    osteps, _ = find_order(on, seed=seed, max_log2_size=max_log2_size)
     cn = tb.Network.from_circuit(circ, diag_hyper=hyper)
     co = tb.Order(cn, seed=seed, max_log2_size=max_log2_size)
     assert co.steps() == osteps                       # bit-identical order
@@ -459,7 +459,7 @@ def test_full_size_config_slices(ci, tgt):
     _cuda()
     c = config_circuit(ci)
     on = build_network(c)
-    osteps, _ = find_order(on, seed=0)
+    osteps, _ = find_order(on, seed=0, max_log2_size=tgt)
     sl = choose_slices(on, osteps, tgt)
     cn = tb.Network.from_circuit(c)
     co = tb.Order(cn, seed=0, max_log2_size=tgt)

@@ -67,7 +67,7 @@ def test_order_and_slices_bit_identical(case):
         c, hyper, seed, tgt = random3d(6, 6, 1, n_patches=1), False, 9, 16
     on, cn = _compare_networks(c, hyper)
     co = tb.Order(cn, seed=seed, max_log2_size=tgt)
-    os_, _ = find_order(on, seed=seed)
+    os_, _ = find_order(on, seed=seed, max_log2_size=tgt)
     assert co.steps() == os_
     if tgt:
         assert co.slices() == choose_slices(on, os_, tgt)
@@ -78,7 +78,7 @@ def test_order_bit_identical_config1():
     c = config_circuit(1)
     on, cn = _compare_networks(c, False)
     co = tb.Order(cn, seed=7, max_log2_size=30)
-    os_, _ = find_order(on, seed=7)
+    os_, _ = find_order(on, seed=7, max_log2_size=30)
     assert co.steps() == os_
     assert co.slices() == choose_slices(on, os_, 30)
 

@@ -12,7 +12,7 @@ from tn_inputs import Circuit, lattice_cz, sycamore, iqp, random3d, inverse_circ
 from tn_inputs.circuits import haar_unitary
 from oracle.network import build_network
 from oracle import ssa
-from oracle.ssa import find_order, step_costs, choose_slices
+from oracle.ssa import find_order, step_costs, choose_slices, sliced_work
 from oracle.contract import contract_tree, contract_pair, contract_pair_loops, kept_per_step, leaf_tensors
 from oracle.statevector import statevector
 from oracle import bounds
@@ -191,6 +191,49 @@ def test_slicing_sums_to_unsliced():
     # every sliced-contraction tensor respects the size target
     kept = kept_per_step(net, steps)
     assert all(sum(net.log2dim(i) for i in kk if i not in sl) <= big - 3 for kk in kept)
+
+
+def test_sliced_work_counts_executed_multiplications():
+    """sliced_work (the R10 / R11 objective) = the multiplications a literal nested-loop
+    execution (Eq. (3): M per step) performs over every slice of the sliced contraction;
+    without slices it is half the Eq. (3) total sum_k 2 M_k."""
+    c = lattice_cz(2, 3, 4, 62)
+    net = build_network(c)
+    steps, _ = find_order(net, seed=0, n_seeds=1)
+    assert sliced_work(net, steps, []) == sum(2.0 ** m for m, _ in step_costs(net, steps))
+    big = max(r for _, r in step_costs(net, steps))
+    sl = choose_slices(net, steps, big - 2)
+    assert len(sl) >= 1
+    kept = kept_per_step(net, steps)
+    x = random_bitstrings(c.n, 1, 4)[0]
+    n = len(net.tensors)
+    muls = 0
+    for vals in itertools.product(*[range(net.dims[i]) for i in sl]):
+        fixed = dict(zip(sl, vals))
+        nodes = dict(enumerate(leaf_tensors(net, x, fixed)))
+        for k, (a, b) in enumerate(steps):
+            (Ai, A), (Bi, B) = nodes.pop(a), nodes.pop(b)
+            kk = [i for i in kept[k] if i not in fixed]
+            _, _, n_mul, _ = contract_pair_loops(Ai, A, Bi, B, kk, net.dims)
+            muls += n_mul
+            nodes[n + k] = contract_pair(Ai, A, Bi, B, kk, net.dims)
+    assert sliced_work(net, steps, sl) == muls
+
+
+def test_find_order_keeps_least_sliced_work():
+    """R10 with a slicing target: the kept hierarchy has the smallest sliced work among
+    the n_seeds candidates (each candidate = the n_seeds=1 hierarchy of its stream)."""
+    c = lattice_cz(4, 4, 8, 63)
+    net = build_network(c)
+    tgt = 8
+    steps, _ = find_order(net, seed=5, n_seeds=3, max_log2_size=tgt)
+    w = sliced_work(net, steps, choose_slices(net, steps, tgt))
+    cands = []
+    for r in range(3):
+        ctx = ssa._Ctx(net, 5, 8, 32, 64, 256)
+        ssa._build(ctx, list(range(len(net.tensors))), 1 + r, 0)
+        cands.append(sliced_work(net, ctx.steps, choose_slices(net, ctx.steps, tgt)))
+    assert w == min(cands)
 
 
 # ------------------------------------------------------------ geometry --------
