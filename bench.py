@@ -41,12 +41,13 @@ ORDER_SEED = 0
 # order (largest tensor of a slice 2^t entries; the first plan that fits HBM is used)
 # n_seeds: randomized separator hierarchies built, the one with the least Eq. (3) work of
 # all slices kept (R10) -- for sliced configs the slicing overhead varies by
-# orders of magnitude between hierarchies (configs[1]: 2^59.2 with 4, 2^56.7 with 64)
+# orders of magnitude between hierarchies (configs[1]: 2^59.2 with 4, 2^56.7 with 64,
+# 2^54.6 with 256; built on host threads, ~10 s)
 SPEC = {
-    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
-    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
+    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
+    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
     3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True, n_seeds=4),
-    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=64),
+    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
 }
 # complex128 GEMM on DMMA: MEASURED_PEAKS.json has no fp64 figure; our own probe
 # (scripts/probes/dmma_peak.cu, profiles/r01/fp64_tensor_peak.md) measured 37.0 TF/s of

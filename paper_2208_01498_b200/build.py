@@ -48,7 +48,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, os.path.basename(s) + ".o")
         if force or _newer([src] + deps, obj):
-            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math", "-Wall",
                   *inc, "-c", src, "-o", obj])
         objs.append(obj)
     for s in CUDA_SRCS:
@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 f.write(out)
         objs.append(obj)
     if force or _newer(objs, LIB):
-        _run([NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcudart"])
+        _run([NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcudart", "-Xcompiler", "-pthread"])
     return LIB
 
 

@@ -4,6 +4,9 @@
 // Compiled with -ffp-contract=off: every floating-point decision is a plain
 // IEEE-754 double operation in a fixed order.
 #include <algorithm>
+#include <atomic>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <map>
 #include <numeric>
@@ -595,36 +598,46 @@ Order find_order(const Network& net, uint64_t seed, const OrderParams& p) {
   // R10: the randomized hierarchy is built n_seeds times; keep the one with the smallest
   // Eq. (3) total -- of all slices when a slicing target is set (the slicer's overhead
   // differs by orders of magnitude between hierarchies of similar unsliced cost)
-  Order best;
-  bool have = false;
-  double best_w = 0.0;
+  // the hierarchies are independent (own root streams): built on host threads, then the
+  // first one with the least work is kept -- the same choice as a serial loop
   std::vector<int> ids(net.tensors.size());
   std::iota(ids.begin(), ids.end(), 0);
-  for (int r = 0; r < p.n_seeds; ++r) {
+  const int R = std::max(1, p.n_seeds);
+  std::vector<Order> cand(R);
+  std::vector<double> work(R, 0.0);
+  auto one = [&](int r) {
     Ctx c(net, seed, p);
     if (!ids.empty()) build(c, ids, (uint64_t)(1 + r));
-    std::vector<int> m, res;
-    costs(net, c.steps, m, res);
+    Order& o = cand[r];
+    costs(net, c.steps, o.step_m, o.step_res);
     double tot = 0.0;
-    for (int mm : m) tot = tot + std::ldexp(1.0, mm + 1);
-    std::vector<int> sl;
-    double w = tot;
+    for (int mm : o.step_m) tot = tot + std::ldexp(1.0, mm + 1);
+    o.total_2M = tot;
+    o.median_fallbacks = c.medians;
+    o.steps = std::move(c.steps);
+    work[r] = tot;
     if (p.max_log2_size > 0) {
-      sl = choose_slices(net, c.steps, p.max_log2_size);
-      w = sliced_work(net, c.steps, sl);
+      o.slices = choose_slices(net, o.steps, p.max_log2_size);
+      work[r] = sliced_work(net, o.steps, o.slices);
     }
-    if (!have || w < best_w) {
-      have = true;
-      best_w = w;
-      best.steps = c.steps;
-      best.step_m = m;
-      best.step_res = res;
-      best.total_2M = tot;
-      best.median_fallbacks = c.medians;
-      best.slices = sl;
-    }
-  }
-  return best;
+  };
+  const int T = std::max(1, std::min<int>(R, (int)std::thread::hardware_concurrency()));
+  std::atomic<int> next{0};
+  std::vector<std::exception_ptr> err(T);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (int r = next++; r < R; r = next++) one(r);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : err) if (e) std::rethrow_exception(e);
+  int best = 0;
+  for (int r = 1; r < R; ++r) if (work[r] < work[best]) best = r;
+  return std::move(cand[best]);
 }
 
 }  // namespace tn
