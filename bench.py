@@ -367,6 +367,15 @@ def run_ours(args):
                 "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
                 "peak_note": f"{peak_src} HBM copy bandwidth; algorithmic bytes = operands + results of each wave",
                 "share_of_step": prof["ms_small"] / ms if ms else None}
+    clocks = clk.summary()
+    if roof["bound"] == "tensor" and dtype == tb.TN_C64 and clocks.get("sm_mhz"):
+        # the measured cuBLAS "sustained" denominator ran at its own power-capped clock; the
+        # tensor pipe's own ceiling at this run's median clock: a 128 x 128 x 16 tcgen05 MMA
+        # every 64 cycles per SM (8192 fp16 flops / clk / SM), 24 fp16 flops per useful 8
+        at_clk = 8192.0 * 148 * clocks["sm_mhz"] * 1e6 / 1e12 / F16_FLOPS_PER_USEFUL
+        roof["clock_ceiling"] = {"sm_mhz": clocks["sm_mhz"], "useful_tflops": at_clk, "frac": gemm_tfs / at_clk,
+                                 "note": "8192 fp16 flops/clk/SM (tcgen05 m128n128k16 floor of 64 cycles) x 148 SMs "
+                                         "x median SM clock of the timed region / 3"}
     if by_slices:
         step_desc = (f"one slice (of 2^{slice_bits}) of one amplitude; rank r takes slices [rK, (r+1)K), "
                      "partial amplitudes summed by one NCCL all-reduce in the timed region")
@@ -393,7 +402,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(nq),
                 "d2h_bytes_per_step": 16},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(c, bits, order.steps(), order.slices(), budget_s=args.cpu_budget,
