@@ -47,7 +47,7 @@ SPEC = {
     1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
     2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
     3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True, n_seeds=4),
-    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
+    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=1024),
 }
 # complex128 GEMM on DMMA: MEASURED_PEAKS.json has no fp64 figure; our own probe
 # (scripts/probes/dmma_peak.cu, profiles/r01/fp64_tensor_peak.md) measured 37.0 TF/s of
