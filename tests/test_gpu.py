@@ -502,6 +502,29 @@ def test_config1_slices_with_bounded_pack_buffers():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+def test_lanes_with_sliced_plan():
+    """Lanes on a sliced plan: every lane walks all slices of its bitstrings (slice
+    counter and fp64 accumulator per lane) -- same amplitudes as one lane, and as the
+    unsliced oracle."""
+    _cuda()
+    c = lattice_cz(5, 5, 8, 4)
+    on = build_network(c)
+    osteps, _ = find_order(on, seed=1, max_log2_size=12)
+    cn = tb.Network.from_circuit(c)
+    co = tb.Order(cn, seed=1, max_log2_size=12)
+    assert co.steps() == osteps
+    plan = tb.Plan(cn, co, dtype=tb.TN_C128)
+    assert plan.info()["n_slices"] > 1
+    bits = random_bitstrings(c.n, 5, 8)
+    single = plan.amplitudes(bits)
+    plan.set_lanes(2)
+    multi = plan.amplitudes(bits)
+    assert np.array_equal(single, multi)
+    for x, g in zip(bits, multi):
+        want = contract_tree(on, osteps, x)
+        assert abs(g - want) <= 1e-10 * max(abs(want), 2.0 ** (-c.n / 2))
+
+
 def test_lanes_concurrent_amplitudes():
     """tn_plan_set_lanes: configs[0] (complex128) and a 6x6 complex64 lattice with
     tensor-core steps, 3 lanes, amplitudes of 7 bitstrings against the oracle (lane j mod 3
