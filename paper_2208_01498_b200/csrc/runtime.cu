@@ -634,7 +634,9 @@ std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& b
 bool want_tc(int dtype, int nb, int m, int n, int k) {
   if (dtype == TN_C128)   // DMMA tiles of 64 x 64 complex, K staged 16 at a time
     return k >= 3 && std::max(m, n) >= 6 && std::min(m, n) >= 5 && (nb + m + n + k) >= 20;
-  return k >= 4 && std::max(m, n) >= 6 && std::min(m, n) >= 4 && (nb + m + n + k) >= 22;
+  // N down to 8 (a 64-wide tile, 1/8 used): for such skinny-N steps with a long K the GEMM
+  // is bound by reading the big operand once, which the tensor-core path does at HBM speed
+  return k >= 4 && std::max(m, n) >= 6 && std::min(m, n) >= 3 && (nb + m + n + k) >= 22;
 }
 // CUDA-core paths for large non-GEMM-shaped steps (skinny.cu): long contraction with
 // few outputs, or short contraction with a large output

@@ -110,6 +110,7 @@ def _gemm_case(nb, m, n, k, perm_seed=None):
 TC_CASES = [
     (0, 7, 7, 4, None),       # exactly one 128x128 tile, K = 16
     (0, 6, 5, 4, None),       # ragged: M = 64 < 128, N = 32 < BN
+    (0, 9, 3, 10, 12),        # skinny N = 8 (one eighth of a 64-wide tile), permuted
     (0, 9, 8, 9, None),       # 4 x 2 tiles, K = 512 (16 stages)
     (2, 7, 6, 5, 3),          # batch 4, permuted layouts folded into the pack
     (0, 10, 10, 12, 5),       # several tiles, K = 4096, permuted
