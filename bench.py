@@ -295,7 +295,10 @@ def run_ours(args):
     flops_step = flops_slice * step_slices
     total_flops = flops_step * args.steps * ws
     value = total_flops / (ms / 1e3)
-    amps_per_s = value / (flops_slice * (2.0 ** slice_bits))
+    # an amplitude = its contributing slices (provably zero ones are skipped by
+    # tn_contract / tn_amplitudes); this rank's first bitstring
+    contrib = plan.contributing_slices(my_bits[0]) if n_slices > 1 else 1
+    amps_per_s = value / (flops_slice * contrib)
 
     # ---- e2e: the public host-buffer call, H2D bits (pinned host memory) + D2H amplitude
     # inside the region ----
@@ -391,7 +394,7 @@ def run_ours(args):
         "config": {"workload": workload_name(ci, c, slice_log2),
                    "step": step_desc, "flops_per_step": flops_step,
                    "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice if flops_slice else None,
-                   "slice_bits": slice_bits,
+                   "slice_bits": slice_bits, "contributing_slices": contrib,
                    "l2": "working set (GB intermediates) >> 126 MB L2, no flush" if pinfo["arena_bytes"] > 1e9
                          else "arena below L2 size: steps re-read warm intermediates (no flush)",
                    "arena_gb": pinfo["arena_bytes"] / 1e9},

@@ -189,6 +189,13 @@ int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_be
  * the lanes concurrently on their own streams (ordered after `stream`).  Synchronizes
  * `stream`. */
 int tn_amplitudes(tn_plan plan, const uint8_t* bits, int32_t n_bits, double* amps, void* stream);
+/* tn_contributing_slices: number of slices of the plan that are not provably zero for the
+ * bitstring (host uint8[n_qubits]): a leaf whose only sliced index is j vanishes for some
+ * values of j given its output bits (e.g. the delta of a CZ bond next to a bound output
+ * leg), and every slice with such a digit contracts to exactly 0.  tn_contract and
+ * tn_amplitudes (host bitstrings) skip those slices; the device-bitstring calls run them.
+ * count saturates at INT64_MAX. */
+int tn_contributing_slices(tn_plan plan, const uint8_t* bits, int64_t* count);
 /* tn_plan_set_lanes: give the plan n_lanes (>= 1) independent copies of its per-
  * contraction device state (arena, pointer table, bitstring / slice / amplitude slots,
  * tensor maps, stream, CUDA graph) so tn_amplitudes contracts n_lanes bitstrings at

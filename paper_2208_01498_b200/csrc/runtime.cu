@@ -755,6 +755,17 @@ struct tn_plan_s {
   int64_t kernels_per_slice = 0;
   std::vector<int32_t> step_table;   // 6 per step: path, nb, m, n, k, launch position
   std::vector<int64_t> node_off;     // arena offset of every intermediate (-1: leaf)
+  // Provably zero slices: a leaf whose only sliced index is j and whose other indices are
+  // output legs (or open bonds) can vanish entirely for some value v of j given the
+  // output bits (e.g. the delta of a CZ bond next to a bound output leg): slices with
+  // that digit contribute exactly 0 and are skipped when the bitstring is on the host.
+  struct Forced {
+    int pos = 0, dim_log2 = 0;
+    std::vector<int> qubits;        // output legs of the leaf (their bits select the row)
+    std::vector<uint8_t> zero;      // zero[(combo << dim_log2) | v]
+  };
+  std::vector<Forced> forced;
+  std::vector<int32_t> sl_shift_h, sl_log2_h;
 
   // Extra lanes (tn_plan_set_lanes): independent copies of the per-contraction state --
   // arena, pointer table, bitstring / slice / amplitude slots, tensor maps, stream and
@@ -1139,6 +1150,35 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
   for (int i : ord.slices) sl_log2.push_back(l2[i]);
   P.slice_bits = sh;
   P.n_slices = sh >= 63 ? INT64_MAX : int64_t(1) << sh;
+  P.sl_shift_h = sl_shift;
+  P.sl_log2_h = sl_log2;
+  for (int t = 0; t < n; ++t) {
+    const auto& T = net.tensors[t];
+    int only = -1, cnt = 0;
+    for (int i : T.inds) if (sliced.count(i)) { only = i; ++cnt; }
+    if (cnt != 1) continue;
+    tn_plan_s::Forced f;
+    f.pos = slice_pos[only];
+    f.dim_log2 = l2[only];
+    std::vector<int> oax;                 // axes of the output legs
+    for (size_t a = 0; a < T.inds.size(); ++a)
+      if (out_q.count(T.inds[a])) { oax.push_back((int)a); f.qubits.push_back(out_q[T.inds[a]]); }
+    const int sax = (int)(std::find(T.inds.begin(), T.inds.end(), only) - T.inds.begin());
+    f.zero.assign(size_t(1) << (f.qubits.size() + f.dim_log2), 1);
+    std::vector<int64_t> st(T.inds.size());
+    int64_t acc = 1;
+    for (int k = (int)T.inds.size() - 1; k >= 0; --k) { st[k] = acc; acc *= net.dims[T.inds[k]]; }
+    for (int64_t e = 0; e < acc; ++e) {
+      if (T.data[e] == tn::cplx(0, 0)) continue;
+      size_t combo = 0;
+      for (size_t q = 0; q < oax.size(); ++q) combo = (combo << 1) | size_t((e / st[oax[q]]) % net.dims[T.inds[oax[q]]] & 1);
+      const int v = (int)((e / st[sax]) % net.dims[only]);
+      f.zero[(combo << f.dim_log2) | v] = 0;
+    }
+    bool any = false;
+    for (uint8_t z : f.zero) any |= z != 0;
+    if (any) P.forced.push_back(std::move(f));
+  }
   P.sl_log2_d = upload(sl_log2);
   P.sl_shift_d = upload(sl_shift);
   CK(cudaMalloc(&P.bits_d, std::max(1, net.n_qubits)));
@@ -1272,16 +1312,55 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
   }
 }
 
+// allowed values of every sliced index for a host bitstring (bit v of mask[j]); a slice
+// with a digit outside its mask contracts to exactly 0 (tn_plan_s::Forced)
+std::vector<uint32_t> slice_masks(const tn_plan_s& P, const uint8_t* bits) {
+  std::vector<uint32_t> m(P.sl_log2_h.size());
+  for (size_t j = 0; j < m.size(); ++j) m[j] = (P.sl_log2_h[j] >= 5) ? 0xffffffffu : (1u << (1 << P.sl_log2_h[j])) - 1;
+  for (const auto& f : P.forced) {
+    size_t combo = 0;
+    for (int q : f.qubits) combo = (combo << 1) | (bits[q] & 1);
+    for (int v = 0; v < (1 << f.dim_log2); ++v)
+      if (f.zero[(combo << f.dim_log2) | v]) m[f.pos] &= ~(1u << v);
+  }
+  return m;
+}
+bool slice_allowed(const tn_plan_s& P, const std::vector<uint32_t>& m, int64_t s) {
+  for (size_t j = 0; j < m.size(); ++j) {
+    const int v = P.sl_shift_h[j] >= 63 ? 0 : (int)((s >> P.sl_shift_h[j]) & ((int64_t(1) << P.sl_log2_h[j]) - 1));
+    if (!((m[j] >> v) & 1)) return false;
+  }
+  return true;
+}
+bool masks_full(const tn_plan_s& P, const std::vector<uint32_t>& m) {
+  for (size_t j = 0; j < m.size(); ++j)
+    if (P.sl_log2_h[j] < 5 && m[j] != (1u << (1 << P.sl_log2_h[j])) - 1) return false;
+  return true;
+}
+
+// graph replays of slices [s0, s1) on `st`; with a host bitstring, provably zero slices
+// are skipped (the slice counter is set before each replay)
 void run_slices(tn_plan_s& P, const uint8_t* bits, bool bits_on_device, int64_t s0, int64_t s1, cudaStream_t st) {
   if (s0 < 0 || s1 > P.n_slices || s0 > s1) throw Err(TN_EINVAL, "slice range out of bounds");
   CK(cudaSetDevice(P.device));
   if (P.net->n_qubits > 0)
     CK(cudaMemcpyAsync(P.bits_d, bits, P.net->n_qubits, bits_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  set_i64_kernel<<<1, 1, 0, st>>>(P.slice_d, s0);
   CK(cudaMemsetAsync(P.amp_d, 0, 16, st));
+  std::vector<uint32_t> m;
+  if (!bits_on_device && !P.forced.empty()) m = slice_masks(P, bits);
+  if (m.empty() || masks_full(P, m)) {
+    set_i64_kernel<<<1, 1, 0, st>>>(P.slice_d, s0);
+    for (int64_t s = s0; s < s1; ++s) {
+      CK(cudaGraphLaunch(P.graph, st));
+      g_launches += P.kernels_per_slice;
+    }
+    return;
+  }
   for (int64_t s = s0; s < s1; ++s) {
+    if (!slice_allowed(P, m, s)) continue;
+    set_i64_kernel<<<1, 1, 0, st>>>(P.slice_d, s);
     CK(cudaGraphLaunch(P.graph, st));
-    g_launches += P.kernels_per_slice;
+    g_launches += P.kernels_per_slice + 1;
   }
 }
 
@@ -1531,9 +1610,16 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
       double2* ad = l ? p->extra[l - 1].amp_d : p->amp_d;
       cudaGraphExec_t gr = l ? p->extra[l - 1].graph : p->graph;
       if (nq > 0) CK(cudaMemcpyAsync(bd, bits_all + (size_t)j * nq, nq, cudaMemcpyDeviceToDevice, ss));
-      set_i64_kernel<<<1, 1, 0, ss>>>(sd, 0);
       CK(cudaMemsetAsync(ad, 0, 16, ss));
+      std::vector<uint32_t> m;
+      if (!p->forced.empty()) m = slice_masks(*p, bits + (size_t)j * nq);
+      const bool full = m.empty() || masks_full(*p, m);
+      if (full) set_i64_kernel<<<1, 1, 0, ss>>>(sd, 0);
       for (int64_t s = 0; s < p->n_slices; ++s) {
+        if (!full) {
+          if (!slice_allowed(*p, m, s)) continue;
+          set_i64_kernel<<<1, 1, 0, ss>>>(sd, s);
+        }
         CK(cudaGraphLaunch(gr, ss));
         g_launches += p->kernels_per_slice;
       }
@@ -1548,6 +1634,17 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
     CK(cudaFreeAsync(res, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaEventDestroy(ready));
+  });
+}
+
+int tn_contributing_slices(tn_plan p, const uint8_t* bits, int64_t* count) {
+  return guard([&] {
+    if (!p || !count || (!bits && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
+    const auto m = slice_masks(*p, bits);
+    double c = 1.0;
+    for (size_t j = 0; j < m.size(); ++j)
+      c *= p->sl_log2_h[j] >= 5 ? std::ldexp(1.0, p->sl_log2_h[j]) : (double)__builtin_popcount(m[j]);
+    *count = c >= 9.2e18 ? INT64_MAX : (int64_t)c;
   });
 }
 

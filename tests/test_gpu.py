@@ -546,3 +546,76 @@ def test_lanes_concurrent_amplitudes():
         for x, g in zip(bits, multi):
             want = contract_tree(on, osteps, x)
             assert abs(g - want) <= tol * max(abs(want), scale)
+
+
+def test_bench_plan_slice_self_consistent():
+    """The bench's own plan (configs[1], best of 256 hierarchies, largest slicing target
+    that fits, 2^30-entry pack cap: K-slabs, row slabs, CTA pairs, persistent tiles) is
+    beyond the oracle; run one of its slices three ways -- default, pack cap 2^28 (other
+    slab structure), single-CTA GEMM (no cta_group::2 / persistent kernels) -- and require
+    agreement to 1e-5 of the RMS slice (child processes: plans of ~180 GB each)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        import numpy as np, paper_2208_01498_b200 as tb
+        from tn_inputs import config_circuit, random_bitstrings
+        c = config_circuit(1)
+        net = tb.Network.from_circuit(c)
+        for tgt in (34, 33, 32, 31):
+            o = tb.Order(net, seed=0, n_seeds=256, max_log2_size=tgt)
+            try:
+                p = tb.Plan(net, o, dtype=tb.TN_C64)
+                break
+            except tb.TnError:
+                continue
+        x = random_bitstrings(c.n, 1, 1)[0]
+        a = p.contract(x, 0, 4)          # 4 slices, half of them provably zero (skipped)
+        print(repr((tgt, p.info()["slice_bits"], a.real, a.imag)))
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for env in ({}, {"TN_PACK_CAP_LOG2": "28"}, {"TN_GEMM_PAIR": "0", "TN_GEMM_PERSIST": "0"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env=dict(os.environ, **env), cwd=root, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        res.append(eval(r.stdout.strip().splitlines()[-1]))
+    tgt, bits = res[0][0], res[0][1]
+    assert all(r[0] == tgt and r[1] == bits for r in res)
+    vals = [complex(r[2], r[3]) for r in res]
+    scale = 2.0 ** (-64 / 2 - bits / 2)
+    assert max(abs(v) for v in vals) > 0
+    for v in vals[1:]:
+        assert abs(v - vals[0]) <= 1e-5 * max(abs(vals[0]), scale), vals
+
+
+def test_zero_slices_skipped():
+    """Provably zero slices (a leaf whose only sliced index is fixed against its bound
+    output legs vanishes): tn_contributing_slices counts fewer slices than the plan has,
+    and tn_contract (host bitstring, skipping them) equals the device-bitstring sum over
+    all slices and the unsliced oracle."""
+    dev = _cuda()
+    found = False
+    for cseed, seed, tgt in ((30, 2, 3), (31, 2, 3)):      # slicing a CZ bond next to an output leg
+        c = lattice_cz(3, 4, 4, cseed)
+        on = build_network(c)
+        osteps, _ = find_order(on, seed=seed, max_log2_size=tgt)
+        cn = tb.Network.from_circuit(c)
+        co = tb.Order(cn, seed=seed, max_log2_size=tgt)
+        assert co.steps() == osteps
+        plan = tb.Plan(cn, co, dtype=tb.TN_C128)
+        ns = plan.info()["n_slices"]
+        for x in random_bitstrings(c.n, 6, seed):
+            k = plan.contributing_slices(x)
+            assert 1 <= k <= ns
+            if k == ns:
+                continue
+            found = True
+            got = plan.contract(x)
+            bits = torch.from_numpy(x).to(dev)
+            amp = torch.zeros(1, dtype=torch.complex128, device=dev)
+            plan.contract_device(bits.data_ptr(), 0, ns, amp.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            want = contract_tree(on, osteps, x)
+            assert abs(got - amp.item()) <= 1e-12 * max(abs(want), 2.0 ** (-c.n / 2))
+            assert abs(got - want) <= 1e-10 * max(abs(want), 2.0 ** (-c.n / 2))
+    assert found, "no plan with provably zero slices in the sample"
