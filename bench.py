@@ -251,12 +251,22 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
+    # steps run contributing slices only (provably zero ones are skipped by tn_contract /
+    # tn_amplitudes, so they are not work an amplitude needs)
+    total_steps = args.steps + args.warmup
+    if by_slices:       # rank r: contributing slices [r K, (r + 1) K) of one amplitude, then warm-ups
+        live = plan.contributing_slice_ids(my_bits[0], 0, (ws + 1) * total_steps)
+        mine = live[rank * args.steps:(rank + 1) * args.steps] + live[ws * args.steps:ws * args.steps + args.warmup]
+    elif n_slices > 1:  # config 1: contributing slices of this rank's first bitstring
+        mine = plan.contributing_slice_ids(my_bits[0], 0, total_steps)
+    else:
+        mine = [0]
+    mine = (mine * (total_steps // max(len(mine), 1) + 1))[:total_steps]
+
     def step_args(j):
-        """(bitstring row, first slice) of this rank's j-th step"""
-        if by_slices:       # rank r: slices [r * K, (r + 1) * K) of one amplitude (+ warm-up offset)
-            return 0, (rank * args.steps + j) % max(n_slices, 1)
-        if n_slices > 1:    # config 1: slices of this rank's first bitstring
-            return 0, j % n_slices
+        """(bitstring row, first slice) of this rank's j-th step (j >= steps: warm-ups)"""
+        if n_slices > 1:
+            return 0, mine[j]
         return j % len(my_bits), 0
 
     for w in range(args.warmup):

@@ -196,6 +196,10 @@ int tn_amplitudes(tn_plan plan, const uint8_t* bits, int32_t n_bits, double* amp
  * tn_amplitudes (host bitstrings) skip those slices; the device-bitstring calls run them.
  * count saturates at INT64_MAX. */
 int tn_contributing_slices(tn_plan plan, const uint8_t* bits, int64_t* count);
+/* tn_contributing_slice_ids: the first (at most cap) contributing slice ids >= slice_begin,
+ * ascending, into host ids[]; *n receives how many were written. */
+int tn_contributing_slice_ids(tn_plan plan, const uint8_t* bits, int64_t slice_begin, int64_t cap, int64_t* ids,
+                              int64_t* n);
 /* tn_plan_set_lanes: give the plan n_lanes (>= 1) independent copies of its per-
  * contraction device state (arena, pointer table, bitstring / slice / amplitude slots,
  * tensor maps, stream, CUDA graph) so tn_amplitudes contracts n_lanes bitstrings at

@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "tn_last_error", "tn_version", "tn_build_network", "tn_network_free", "tn_network_get_info",
     "tn_network_dims", "tn_network_tensor", "tn_order_params_default", "tn_find_order", "tn_order_free",
     "tn_order_get_info", "tn_order_steps", "tn_order_slices", "tn_plan_create", "tn_plan_free",
-    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_amplitudes", "tn_contract_pair",
+    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_amplitudes", "tn_contract_pair",
     "tn_kernel_launches",
 ]
 
@@ -80,6 +80,7 @@ def _load():
         "tn_plan_steps": (C.c_int, [P, P]),
         "tn_plan_set_lanes": (C.c_int, [P, I32]),
         "tn_contributing_slices": (C.c_int, [P, P, C.POINTER(C.c_int64)]),
+        "tn_contributing_slice_ids": (C.c_int, [P, P, I64, I64, P, C.POINTER(C.c_int64)]),
         "tn_contract": (C.c_int, [P, P, I64, I64, P, P]),
         "tn_contract_device": (C.c_int, [P, P, I64, I64, P, P]),
         "tn_contract_profiled": (C.c_int, [P, P, I64, I64, P, P, C.POINTER(Profile)]),
@@ -230,6 +231,14 @@ class Plan:
         c = C.c_int64()
         _check(lib.tn_contributing_slices(self.h, _ptr(b), C.byref(c)))
         return int(c.value)
+
+    def contributing_slice_ids(self, bits, slice_begin=0, cap=64):
+        """tn_contributing_slice_ids: first `cap` contributing slice ids >= slice_begin."""
+        b = np.ascontiguousarray(bits, dtype=np.uint8)
+        out = np.zeros(max(int(cap), 1), np.int64)
+        c = C.c_int64()
+        _check(lib.tn_contributing_slice_ids(self.h, _ptr(b), int(slice_begin), int(cap), _ptr(out), C.byref(c)))
+        return [int(v) for v in out[:c.value]]
 
     def set_lanes(self, n_lanes):
         """tn_plan_set_lanes: n_lanes concurrent copies of the per-contraction state."""

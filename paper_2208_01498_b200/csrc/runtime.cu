@@ -1648,6 +1648,19 @@ int tn_contributing_slices(tn_plan p, const uint8_t* bits, int64_t* count) {
   });
 }
 
+int tn_contributing_slice_ids(tn_plan p, const uint8_t* bits, int64_t slice_begin, int64_t cap, int64_t* ids,
+                              int64_t* n) {
+  return guard([&] {
+    if (!p || !n || cap < 0 || (cap > 0 && !ids) || (!bits && p->net->n_qubits > 0) || slice_begin < 0)
+      throw Err(TN_EINVAL, "null");
+    const auto m = slice_masks(*p, bits);
+    int64_t k = 0;
+    for (int64_t s = slice_begin; s < p->n_slices && k < cap; ++s)
+      if (slice_allowed(*p, m, s)) ids[k++] = s;
+    *n = k;
+  });
+}
+
 int tn_plan_set_lanes(tn_plan p, int32_t n_lanes) {
   return guard([&] {
     if (!p || n_lanes < 1) throw Err(TN_EINVAL, "tn_plan_set_lanes: bad arguments");
