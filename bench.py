@@ -417,7 +417,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:      # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline_sample(c, bits, order.steps(), order.slices(), budget_s=args.cpu_budget,
                                                    hyper=spec["hyper"])
     print(json.dumps(line))
