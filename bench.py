@@ -67,32 +67,69 @@ def load_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock and clock-event reasons sampled DURING the timed region: an NVML polling
+    thread (5 ms period) that has taken its first sample before __enter__ returns, so
+    even a region of a few milliseconds gets samples (nvidia-smi -lms needs ~0.1 s to
+    start).  Falls back to an nvidia-smi subprocess if NVML is unavailable."""
 
-    def __init__(self, index=0):
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    MASKS = [0x8, 0x40, 0x20, 0x4]      # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
+
+    def __init__(self, index=0, period_s=0.005):
         self.index = index
-        self.rows = []
+        self.period = period_s
+        self.rows = []                  # (sm_mhz, max_mhz, reasons bitmask)
         self.proc = None
+        self.stop = threading.Event()
+        self.t = None
+
+    def _poll(self, nv, h, first):
+        while True:
+            try:
+                self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:
+                pass
+            first.set()
+            if self.stop.wait(self.period):
+                return
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            first = threading.Event()
+            self.t = threading.Thread(target=self._poll, args=(nv, h, first), daemon=True)
+            self.t.start()
+            first.wait(2.0)
+            return self
+        except Exception:
+            self.t = None
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+            r = [v.strip() for v in line.split(",")]
+            if len(r) >= 6 and r[0].replace(".", "").isdigit() and r[1].replace(".", "").isdigit():
+                mask = sum(m for m, v in zip(self.MASKS, r[2:6]) if v == "Active")
+                self.rows.append((float(r[0]), float(r[1]), mask))
 
     def __exit__(self, *a):
+        if self.t is not None:
+            self.stop.set()
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,12 +138,11 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        rows = list(self.rows)
+        sm = [r[0] for r in rows]
+        reasons = sorted({n for r in rows for n, m in zip(self.NAMES, self.MASKS) if r[2] & m})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(r[1] for r in rows) if rows else None,
+                "reasons": reasons, "samples": len(rows), "sampler": "nvml" if self.t is not None else "nvidia-smi"}
 
 
 def dist_env():

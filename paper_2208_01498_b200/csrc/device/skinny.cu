@@ -16,7 +16,7 @@ namespace tnd {
 // Output planes [b][2][rows][K] of R: (re plane, im plane); the host built tile_dst /
 // q_hi for 2 planes per batch (see PackDesc).
 template <typename R>
-__global__ void __launch_bounds__(PACK_THREADS, 4) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 3) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    R* __restrict__ out, int64_t src_base) {
   using C2 = typename cplx_t<R>::type;
@@ -36,35 +36,48 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_planar_kernel(const void
   const int q0 = threadIdx.x * 8;
   const bool writer = q0 < T;
   const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t sb = gmap(tab, d.tile_src, tile);
-    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
-    C2 v[PACK_PER_THREAD];
+  // software pipeline (as pack_f16x2s_kernel): the next tile's loads are in flight while
+  // this tile goes through shared memory and out
+  C2 v[PACK_PER_THREAD];
+  if ((int64_t)blockIdx.x < n_tiles) {
+    const int64_t sb = gmap(tab, d.tile_src, blockIdx.x);
 #pragma unroll
     for (int i = 0; i < PACK_PER_THREAD; ++i)
-      if (threadIdx.x + i * PACK_THREADS < T) v[i] = src[sb + so[i]];
+      if (threadIdx.x + i * PACK_THREADS < T) v[i] = __ldg(src + sb + so[i]);
+  }
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
 #pragma unroll
     for (int i = 0; i < PACK_PER_THREAD; ++i)
       if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
     __syncthreads();
-    __align__(16) R re[8];
-    __align__(16) R im[8];
+    if (tile + gridDim.x < n_tiles) {
+      const int64_t sb = gmap(tab, d.tile_src, tile + gridDim.x);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const C2 w = writer ? s[pack_slot(q0 + j)] : C2{0, 0};
-      re[j] = w.x;
-      im[j] = w.y;
+      for (int i = 0; i < PACK_PER_THREAD; ++i)
+        if (threadIdx.x + i * PACK_THREADS < T) v[i] = __ldg(src + sb + so[i]);
     }
-    __syncthreads();
-    if (!writer) continue;
-    // 8 consecutive elements per plane: two float4 / four double2 stores
+    // 8 consecutive elements per plane leave as two float4 / four double2 stores; the
+    // barrier that frees s for the next tile comes after them
     constexpr int V = 16 / sizeof(R);
     using V4 = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
+    if (writer) {
 #pragma unroll
-    for (int j = 0; j < 8; j += V) {
-      *reinterpret_cast<V4*>(out + db + j) = *reinterpret_cast<const V4*>(&re[j]);
-      *reinterpret_cast<V4*>(out + db + d.plane + j) = *reinterpret_cast<const V4*>(&im[j]);
+      for (int j = 0; j < 8; j += V) {
+        V4 re, im;
+        R* rp = reinterpret_cast<R*>(&re);
+        R* ip = reinterpret_cast<R*>(&im);
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const C2 w = s[pack_slot(q0 + j + u)];
+          rp[u] = w.x;
+          ip[u] = w.y;
+        }
+        *reinterpret_cast<V4*>(out + db + j) = re;
+        *reinterpret_cast<V4*>(out + db + d.plane + j) = im;
+      }
     }
+    __syncthreads();
   }
 }
 

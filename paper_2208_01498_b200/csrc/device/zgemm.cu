@@ -11,57 +11,8 @@
 
 namespace tnd {
 
-// ------------------------------------------------------------- fp64 pack -----
-// Same bit-permutation tiling as pack_f16x2s_kernel (see PackDesc); output planes
-// [b][2][rows][K] complex128 -> (re plane, im plane) of fp64.
-__global__ void __launch_bounds__(PACK_THREADS, 4) pack_f64x2_kernel(const void* const* __restrict__ ptrs, PackDesc d,
-                                                                  const int64_t* __restrict__ tab,
-                                                                  double* __restrict__ out, int64_t src_base) {
-  __shared__ __align__(16) double2 s[1 << PACK_MAX_T];
-  const double2* __restrict__ src = reinterpret_cast<const double2*>(ptrs[d.src]) + src_base;
-  const int64_t n_tiles = int64_t(1) << d.tile_bits;
-  const int64_t lmask = (int64_t(1) << d.ld) - 1;
-  const int T = 1 << d.t_bits;
-  int64_t so[PACK_PER_THREAD];
-  int sl[PACK_PER_THREAD];
-#pragma unroll
-  for (int i = 0; i < PACK_PER_THREAD; ++i) {
-    const int e = threadIdx.x + i * PACK_THREADS;
-    so[i] = e < T ? __ldg(tab + d.e_src + e) : 0;
-    sl[i] = e < T ? pack_slot((int)__ldg(tab + d.e_q + e)) : 0;
-  }
-  const int q0 = threadIdx.x * 8;
-  const bool writer = q0 < T;
-  // destination offsets of the packed layout are in units of one fp64 plane element;
-  // the host built tile_dst / q_hi for 2 planes per batch
-  const int64_t dq = writer ? (q0 & lmask) + gmap(tab, d.q_hi, q0 >> d.ld) : 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t sb = gmap(tab, d.tile_src, tile);
-    const int64_t db = gmap(tab, d.tile_dst, tile) + dq;
-    double2 v[PACK_PER_THREAD];
-#pragma unroll
-    for (int i = 0; i < PACK_PER_THREAD; ++i)
-      if (threadIdx.x + i * PACK_THREADS < T) v[i] = src[sb + so[i]];
-#pragma unroll
-    for (int i = 0; i < PACK_PER_THREAD; ++i)
-      if (threadIdx.x + i * PACK_THREADS < T) s[sl[i]] = v[i];
-    __syncthreads();
-    double re[8], im[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double2 w = writer ? s[pack_slot(q0 + j)] : double2{0.0, 0.0};
-      re[j] = w.x;
-      im[j] = w.y;
-    }
-    __syncthreads();
-    if (!writer) continue;
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      *reinterpret_cast<double2*>(out + db + j) = double2{re[j], re[j + 1]};
-      *reinterpret_cast<double2*>(out + db + d.plane + j) = double2{im[j], im[j + 1]};
-    }
-  }
-}
+// DMMA operands are packed by pack_planar_kernel<double> (skinny.cu): planes
+// [b][2][rows][K] (re plane, im plane) of fp64.
 
 // ------------------------------------------------------------------ DMMA -----
 namespace zg {

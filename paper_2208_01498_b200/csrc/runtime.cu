@@ -263,7 +263,7 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
   if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("f64 pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   for (const PackDesc* d : {&t.px, &t.py}) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d->tile_bits, 148 * 8);
-    tnd::pack_f64x2_kernel<<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
+    tnd::pack_planar_kernel<double><<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
         ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)), 0);
     g_launches++;
   }
@@ -518,7 +518,7 @@ void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaS
 }
 
 // Pack descriptor: bit permutation from the operand's stored layout to [b][rows][k]
-// (destination planes [b][planes][rows][k]); see pack_f16x2s_kernel / pack_f64x2_kernel.
+// (destination planes [b][planes][rows][k]); see pack_f16x2s_kernel / pack_planar_kernel.
 // k_lo < k bits: only the lowest k_lo bits of the k group are packed (a K-slab); the
 // source offsets of the remaining high k bits, one per slab, are appended to `slabs`.
 PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::vector<int>& batch,
