@@ -405,12 +405,15 @@ def run_ours(args):
                 "frac": gemm_tfs / peak_tc if peak_tc else None, "traffic": None, "kernel": kname,
                 "peak_note": pnote, "share_of_step": prof["ms_gemm"] / ms if ms else None}
         if dtype == tb.TN_C64:
-            # DRAM traffic of one representative launch from the committed ncu --set full
-            # capture (the bench's own launches vary in shape): operands are re-read ~3x
-            # from DRAM, harmless for a tensor-bound kernel (DRAM at 11%)
-            roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[8192][8192] = A[8192][4096] B[4096][8192]",
-                                     "dram_bytes": 3.757e9, "algorithmic_bytes": 1.074e9,
-                                     "source": "profiles/r01/ncu_full_summary.md"}
+            # DRAM traffic (bytes) of one launch of the bench's dominant GEMM shape from the
+            # committed ncu --set full capture: a K-slab of the (18, 12, 16) steps (64% of a
+            # configs[1] step).  A is re-read ~8x from DRAM (L2 hit 74%), harmless for a
+            # tensor-bound kernel (DRAM at 13%)
+            roof["traffic"] = 6.935e10 + 8.796e9
+            roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[2^18][2^12] = A[2^18][2^12] B[2^12][2^12] "
+                                               "(one K-slab of the configs[1] (18, 12, 16) steps)",
+                                     "dram_bytes": 6.935e10 + 8.796e9, "algorithmic_bytes": 1.731e10,
+                                     "tensor_active": 0.931, "source": "profiles/r01/ncu_full_summary.md"}
     else:
         roof = {"bound": "hbm", "achieved": small_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
