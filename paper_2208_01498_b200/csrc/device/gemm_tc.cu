@@ -216,6 +216,24 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
+// explicit shared / global vector accesses for the C staging (a generic pointer into the
+// dynamic smem window compiles to generic LD.E / ST.E)
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stg128(void* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 ldg128(const void* p) {
+  float4 v;
+  asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
 // plain bulk copy global -> shared (16-byte aligned, size a multiple of 16)
 __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -354,22 +372,22 @@ __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, 
     // Coalesced C: the warp's 32 x 64 complex block goes through shared memory (the
     // operand stages: every MMA has completed, so they are free) and leaves one 512-byte
     // row per instruction (thread-per-row stores would scatter 32 rows per instruction).
-    float* stg = stage_smem + warp * (32 * EPI_PITCH);
+    const uint32_t stg = smem_u32(stage_smem + warp * (32 * EPI_PITCH));
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      *reinterpret_cast<float4*>(stg + lane * EPI_PITCH + 4 * j) = make_float4(ar[2 * j], ai[2 * j], ar[2 * j + 1], ai[2 * j + 1]);
+      sts128(stg + 4 * (lane * EPI_PITCH + 4 * j), make_float4(ar[2 * j], ai[2 * j], ar[2 * j + 1], ai[2 * j + 1]));
     __syncwarp();
     const int rbase = row0 + lg * 32;
 #pragma unroll 4
     for (int r = 0; r < 32; ++r) {
       if (rbase + r >= M) break;
-      float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_PITCH + 4 * lane);
+      float4 v = lds128(stg + 4 * (r * EPI_PITCH + 4 * lane));
       float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * c_rows + c_row_off + rbase + r) * (int64_t)N + col0) + lane;
       if (acc_c) {
-        const float4 o = *dst;
+        const float4 o = ldg128(dst);
         v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
       }
-      *dst = v;
+      stg128(dst, v);
     }
     return;
   }
@@ -935,25 +953,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
       else { C = reinterpret_cast<float2*>(ptrs[c_node]); c_rows = M_c; c_row_off = m_off; }
       const bool acc_c = accumulate && !partial;
       const int rbase = row0 + lg * 32, col0 = n_blk * CF::BN + ch * 64;
+      const uint32_t stg_u = smem_u32(my_stg);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          *reinterpret_cast<float4*>(my_stg + lane * Cfg2P::STG_PITCH + 4 * j) =
-              make_float4(ar[8 * q + 2 * j], ai[8 * q + 2 * j], ar[8 * q + 2 * j + 1], ai[8 * q + 2 * j + 1]);
+          sts128(stg_u + 4 * (lane * Cfg2P::STG_PITCH + 4 * j),
+                 make_float4(ar[8 * q + 2 * j], ai[8 * q + 2 * j], ar[8 * q + 2 * j + 1], ai[8 * q + 2 * j + 1]));
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = i * 8 + (lane >> 2);
           if (rbase + r < M) {
-            float4 v = *reinterpret_cast<const float4*>(my_stg + r * Cfg2P::STG_PITCH + 4 * (lane & 3));
+            float4 v = lds128(stg_u + 4 * (r * Cfg2P::STG_PITCH + 4 * (lane & 3)));
             float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * c_rows + c_row_off + rbase + r) * (int64_t)N +
                                                     col0 + 8 * q) + (lane & 3);
             if (acc_c) {
-              const float4 o = *dst;
+              const float4 o = ldg128(dst);
               v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
             }
-            *dst = v;
+            stg128(dst, v);
           }
         }
         __syncwarp();
