@@ -629,3 +629,26 @@ def test_zero_slices_skipped():
             assert abs(got - amp.item()) <= 1e-12 * max(abs(want), 2.0 ** (-c.n / 2))
             assert abs(got - want) <= 1e-10 * max(abs(want), 2.0 ** (-c.n / 2))
     assert found, "no plan with provably zero slices in the sample"
+
+
+def test_degenerate_circuits_on_gpu():
+    """Degenerate circuits (one qubit, product state, no gates, disconnected components;
+    tests/degenerate.py) in both dtypes: every amplitude against its closed form and
+    the oracle, and an empty slice range contributes exactly 0."""
+    _cuda()
+    from degenerate import degenerate_circuits, all_bitstrings
+    for c, amp in degenerate_circuits():
+        on = build_network(c)
+        osteps, _ = find_order(on, seed=0)
+        cn = tb.Network.from_circuit(c)
+        co = tb.Order(cn, seed=0)
+        assert co.steps() == osteps
+        xs = all_bitstrings(c.n)
+        for dtype in (tb.TN_C128, tb.TN_C64):
+            plan = tb.Plan(cn, co, dtype=dtype)
+            got = plan.amplitudes(xs)
+            tol = 1e-12 if dtype == tb.TN_C128 else 1e-6
+            for x, g in zip(xs, got):
+                assert abs(g - amp(x)) <= tol, (c.name, dtype, x, g, amp(x))
+                assert abs(g - contract_tree(on, osteps, x)) <= tol
+                assert plan.contract(x, 0, 0) == 0

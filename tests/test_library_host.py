@@ -91,3 +91,14 @@ def test_order_info_consistent():
     assert inf["n_steps"] == cn.info()["n_tensors"] - 1
     assert inf["n_slice_assignments"] == 2 ** inf["n_slices"]
     assert inf["log2_slice_2M"] <= inf["log2_total_2M"] + 1e-9
+
+
+def test_degenerate_networks_and_orders_identical():
+    """Degenerate circuits (tests/degenerate.py: one qubit, product state, no gates,
+    disconnected components): the C++ network and order equal the oracle's."""
+    from degenerate import degenerate_circuits
+    for c, _ in degenerate_circuits():
+        on, cn = _compare_networks(c, False)
+        co = tb.Order(cn, seed=0)
+        os_, _ = find_order(on, seed=0)
+        assert co.steps() == os_, c.name

@@ -373,3 +373,19 @@ def test_theorem_constants():
     assert abs(bounds.a_d(2) - (4 + 2 * math.sqrt(3))) < 1e-12
     assert abs(bounds.a2_prime() - 5.3705) < 1e-3 and bounds.a2_prime() < bounds.a_d(2)
     assert abs(1 / math.log2(1.5) - 1.7095112913514547) < 1e-12
+
+
+# ------------------------------------------------------------ degenerate ------
+def test_degenerate_circuits_closed_forms():
+    """A single qubit, a product state, no gates, two disconnected components: the
+    oracle's network + tree contraction equals the closed-form amplitude for every
+    bitstring (tests/degenerate.py)."""
+    from degenerate import degenerate_circuits, all_bitstrings
+    from oracle.contract import contract_tree
+    for c, amp in degenerate_circuits():
+        on = build_network(c)
+        steps, _ = ssa.find_order(on, seed=0)
+        for x in all_bitstrings(c.n):
+            want = amp(x)
+            got = contract_tree(on, steps, x)
+            assert abs(got - want) <= 1e-12, (c.name, x, got, want)
