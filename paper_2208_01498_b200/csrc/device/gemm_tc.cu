@@ -744,8 +744,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
 // dedicated 20 KB staging area (8 complex per row per round, 64-byte row segments), the
 // operand stages being busy with the next tile.
 struct Cfg2P {
-  static constexpr int STG_PITCH = 20;                                 // floats per staged row (8 complex + pad)
-  static constexpr int STG_BYTES = Cfg2::EPI_WARPS * 32 * STG_PITCH * 4;
+  static constexpr int STG_PITCH = 68;                                 // floats per staged row (32 complex + pad)
+  static constexpr int STG_BYTES = Cfg2::EPI_WARPS * 8 * STG_PITCH * 4;
   static constexpr int SMEM = Cfg2::STAGES * Cfg2::STAGE + Cfg2::SLOTS * Cfg2::SC_BYTES + STG_BYTES + 1024 + 512;
 };
 
@@ -900,7 +900,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     // ---- epilogue warps ----
     const int lg = warp & 3, ch = warp >> 2;
     const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
-    float* my_stg = stg + warp * (32 * Cfg2P::STG_PITCH);
+    float* my_stg = stg + warp * (8 * Cfg2P::STG_PITCH);
     int gp = 0;
     for (int tile = pair; tile < total; tile += n_pairs) {
       int b, split, m_blk, n_blk;
@@ -945,8 +945,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
           mbar_arrive(&sempty[slot]);
         }
       }
-      // C tile rows [row0 + 32 lg, +32) x columns [n_blk 128 + 64 ch, +64): 8 rounds of
-      // 8 complex per row through the staging area, 4 lanes x 16 B per 64-byte row segment
+      // C tile rows [row0 + 32 lg, +32) x columns [n_blk 128 + 64 ch, +64) in 8 rounds of
+      // 8 rows x 32 complex: the 8 lanes owning the rows stage 256 B each, then 16 lanes
+      // per row store whole 256-byte row segments (2 rows, 4 full lines per instruction)
       float2* C;
       int c_rows, c_row_off;
       if (partial) { C = partial + (int64_t)split * nb * M * (int64_t)N; c_rows = M; c_row_off = 0; }
@@ -954,20 +955,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
       const bool acc_c = accumulate && !partial;
       const int rbase = row0 + lg * 32, col0 = n_blk * CF::BN + ch * 64;
       const uint32_t stg_u = smem_u32(my_stg);
+      constexpr int P = Cfg2P::STG_PITCH;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int g = 0; g < 4; ++g)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          sts128(stg_u + 4 * (lane * Cfg2P::STG_PITCH + 4 * j),
-                 make_float4(ar[8 * q + 2 * j], ai[8 * q + 2 * j], ar[8 * q + 2 * j + 1], ai[8 * q + 2 * j + 1]));
+      for (int h = 0; h < 2; ++h) {
+        if ((lane >> 3) == g) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            sts128(stg_u + 4 * ((lane & 7) * P + 4 * j),
+                   make_float4(ar[32 * h + 2 * j], ai[32 * h + 2 * j], ar[32 * h + 2 * j + 1], ai[32 * h + 2 * j + 1]));
+        }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int r = i * 8 + (lane >> 2);
+          const int rr = 2 * i + (lane >> 4), r = 8 * g + rr;
           if (rbase + r < M) {
-            float4 v = lds128(stg_u + 4 * (r * Cfg2P::STG_PITCH + 4 * (lane & 3)));
+            float4 v = lds128(stg_u + 4 * (rr * P + 4 * (lane & 15)));
             float4* dst = reinterpret_cast<float4*>(C + ((int64_t)b * c_rows + c_row_off + rbase + r) * (int64_t)N +
-                                                    col0 + 8 * q) + (lane & 3);
+                                                    col0 + 32 * h) + (lane & 15);
             if (acc_c) {
               const float4 o = ldg128(dst);
               v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
