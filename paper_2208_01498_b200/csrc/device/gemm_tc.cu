@@ -163,7 +163,12 @@ namespace tc {
 constexpr int BM = 128;    // rows per tile (TMEM lanes)
 constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
 constexpr int PROMO = 2;   // stages per TMEM accumulation = one 64-element scale chunk
-constexpr int GROUP_M = 8; // CTA rasterization: 8 M-tiles share each B panel in flight
+// CTA rasterization: GROUP_M M-tiles sweep the N tiles together (panels shared in L2).
+// Pair kernel: 4 (measured, scripts/raster_sweep.sh: DRAM reads 67 -> 55 GB on a
+// (2^18, 2^12, 2^12) step, 1-2% faster through the power-capped clock); single-CTA and
+// persistent kernels: 8 (the persistent short-K tiles prefer 8).
+constexpr int GROUP_M = 8, GROUP_M_PAIR = 4;
+__device__ int d_group_m = 0;   // > 0: TN_GEMM_GROUP_M override (raster experiments)
 
 template <int BN>
 struct Cfg {
@@ -500,11 +505,12 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   // tile rasterization: groups of GROUP_M M-tiles sweep the N-tiles together (L2 reuse)
   const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BN - 1) / BN;
   const int pid = blockIdx.x;
-  const int group = pid / (GROUP_M * n_tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gm = min(n_tiles_m - first_m, GROUP_M);
-  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
-  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+  const int group_m = d_group_m > 0 ? d_group_m : GROUP_M;
+  const int group = pid / (group_m * n_tiles_n);
+  const int first_m = group * group_m;
+  const int gm = min(n_tiles_m - first_m, group_m);
+  const int m_blk = first_m + (pid % (group_m * n_tiles_n)) % gm;
+  const int n_blk = (pid % (group_m * n_tiles_n)) / gm;
   // split-K: blockIdx.z = split * nb + batch; this CTA covers K chunks [kc0, kc0 + nk)
   const int b = blockIdx.z % nb, split = blockIdx.z / nb;
   const int nk_all = (K + BK - 1) / BK;
@@ -660,11 +666,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   // pair rasterization: groups of GROUP_M 256-row tiles sweep the N tiles together
   const int n_tiles_m = (M + 255) / 256, n_tiles_n = N / CF::BN;
   const int pid = blockIdx.x >> 1;
-  const int group = pid / (GROUP_M * n_tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gm = min(n_tiles_m - first_m, GROUP_M);
-  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
-  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+  const int group_m = d_group_m > 0 ? d_group_m : GROUP_M_PAIR;
+  const int group = pid / (group_m * n_tiles_n);
+  const int first_m = group * group_m;
+  const int gm = min(n_tiles_m - first_m, group_m);
+  const int m_blk = first_m + (pid % (group_m * n_tiles_n)) % gm;
+  const int n_blk = (pid % (group_m * n_tiles_n)) / gm;
   const int row0 = m_blk * 256 + (int)rank * BM;
   const int b = blockIdx.z % nb, split = blockIdx.z / nb;
   const int nk_all = (K + BK - 1) / BK;
@@ -833,11 +840,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     const int z = tile / tiles_per_z, pid = tile % tiles_per_z;
     b = z % nb;
     split = z / nb;
-    const int group = pid / (GROUP_M * n_tiles_n);
-    const int first_m = group * GROUP_M;
-    const int gm = min(n_tiles_m - first_m, GROUP_M);
-    m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gm;
-    n_blk = (pid % (GROUP_M * n_tiles_n)) / gm;
+    const int group_m = d_group_m > 0 ? d_group_m : GROUP_M;
+    const int group = pid / (group_m * n_tiles_n);
+    const int first_m = group * group_m;
+    const int gm = min(n_tiles_m - first_m, group_m);
+    m_blk = first_m + (pid % (group_m * n_tiles_n)) % gm;
+    n_blk = (pid % (group_m * n_tiles_n)) / gm;
   };
 
   if (warp == TMA_WARP && lane == 0) {

@@ -339,6 +339,15 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
 
 void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                Marks* mk = nullptr) {
+  static bool group_set = [] {      // TN_GEMM_GROUP_M: M tiles per raster group (experiments)
+    const char* e = std::getenv("TN_GEMM_GROUP_M");
+    if (e && std::atoi(e) > 0) {
+      const int g = std::atoi(e);
+      CK(cudaMemcpyToSymbol(tnd::tc::d_group_m, &g, sizeof(int)));
+    }
+    return true;
+  }();
+  (void)group_set;
   if (t.kind == K_DMMA) return launch_dmma(t, arena, ptrs_d, tab_d, st, mk);
   if (t.kind == K_SKINNY || t.kind == K_WIDE) {
     if (t.esz == 8) return launch_cuda_core<float>(t, arena, ptrs_d, tab_d, st, mk);
