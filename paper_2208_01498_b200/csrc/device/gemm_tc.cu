@@ -164,10 +164,11 @@ constexpr int BM = 128;    // rows per tile (TMEM lanes)
 constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
 constexpr int PROMO = 2;   // stages per TMEM accumulation = one 64-element scale chunk
 // CTA rasterization: GROUP_M M-tiles sweep the N tiles together (panels shared in L2).
-// Pair kernel: 4 (measured, scripts/raster_sweep.sh: DRAM reads 67 -> 55 GB on a
-// (2^18, 2^12, 2^12) step, 1-2% faster through the power-capped clock); single-CTA and
-// persistent kernels: 8 (the persistent short-K tiles prefer 8).
-constexpr int GROUP_M = 8, GROUP_M_PAIR = 4;
+// Measured with scripts/raster_sweep.sh (DRAM traffic costs clock under the power cap):
+// pair kernel 4 (DRAM reads 67 -> 55 GB on a (2^18, 2^12, 2^12) step, 1-2% faster);
+// persistent short-K pair kernel 32 (69 -> 40 GB on (2^18, 2^16, 2^8), 0.5-1.3% faster);
+// single-CTA kernel 8.
+constexpr int GROUP_M = 8, GROUP_M_PAIR = 4, GROUP_M_PERSIST = 32;
 __device__ int d_group_m = 0;   // > 0: TN_GEMM_GROUP_M override (raster experiments)
 
 template <int BN>
@@ -840,7 +841,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     const int z = tile / tiles_per_z, pid = tile % tiles_per_z;
     b = z % nb;
     split = z / nb;
-    const int group_m = d_group_m > 0 ? d_group_m : GROUP_M;
+    const int group_m = d_group_m > 0 ? d_group_m : GROUP_M_PERSIST;
     const int group = pid / (group_m * n_tiles_n);
     const int first_m = group * group_m;
     const int gm = min(n_tiles_m - first_m, group_m);
