@@ -240,6 +240,19 @@ __device__ __forceinline__ float4 ldg128(const void* p) {
   asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
   return v;
 }
+// TMA tensor store / reduce-add of a staged smem box (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(smem), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(smem), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // plain bulk copy global -> shared (16-byte aligned, size a multiple of 16)
 __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -329,7 +342,7 @@ template <int BN, bool kPair>
 __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
                                          uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int n_promo,
                                          float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c,
-                                         int c_rows, int c_row_off) {
+                                         int c_rows, int c_row_off, const CUtensorMap* tmC = nullptr) {
   using CF = Cfg<BN>;
   const int lg = warp & 3;                 // TMEM lane group (rows 32 lg .. 32 lg + 31)
   const int ch = warp >> 2;                // column half: columns [64 ch, 64 ch + 64)
@@ -374,6 +387,33 @@ __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, 
     }
   }
   const int col0 = col0_blk + ch * 64;
+  if (tmC) {
+    // TMA tensor stores (reduce-add for C += of K-slabs): the warp's 32 x 64 complex block
+    // goes to the (idle) operand stages as 4 boxes of 32 rows x 16 complex in the
+    // SWIZZLE_128B layout of the C map (16-byte chunk j of row r at j ^ (r & 7)); one lane
+    // issues the 4 stores.  Full tiles only (pair kernel: M % 256 == 0, N % 128 == 0).
+    const uint32_t stg = smem_u32(stage_smem) + warp * (4 * 32 * 128);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        sts128(stg + q * (32 * 128) + lane * 128 + ((j ^ (lane & 7)) << 4),
+               make_float4(ar[16 * q + 2 * j], ai[16 * q + 2 * j], ar[16 * q + 2 * j + 1], ai[16 * q + 2 * j + 1]));
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      const int y = b * c_rows + c_row_off + row0 + lg * 32;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (acc_c) tma_reduce_add_2d(tmC, stg + q * (32 * 128), 2 * (col0 + 16 * q), y);
+        else tma_store_2d(tmC, stg + q * (32 * 128), 2 * (col0 + 16 * q), y);
+      }
+      bulk_commit();
+      bulk_wait_all();
+    }
+    __syncwarp();
+    return;
+  }
   if (col0 + 64 <= N) {
     // Coalesced C: the warp's 32 x 64 complex block goes through shared memory (the
     // operand stages: every MMA has completed, so they are free) and leaves one 512-byte
@@ -648,7 +688,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
                          const float* __restrict__ scA, const float* __restrict__ scB,
                          void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
                          int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate,
-                         int32_t m_off, int32_t M_c) {
+                         int32_t m_off, int32_t M_c, const __grid_constant__ CUtensorMap tmC) {
   using CF = Cfg2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -731,7 +771,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   } else {
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
     epilogue<128, true>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
-                        n_blk * CF::BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off);
+                        n_blk * CF::BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off,
+                        partial ? nullptr : &tmC);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -749,12 +790,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
 // epilogue has released -- the per-CTA prologue/fill/drain of the one-tile-per-CTA
 // kernel (a third of the time of a K = 256 step) disappears.  All three roles walk the
 // same tile sequence with global stage / promotion counters.  C leaves through a
-// dedicated 20 KB staging area (8 complex per row per round, 64-byte row segments), the
-// operand stages being busy with the next tile.
+// dedicated 64 KB staging area by TMA tensor stores (reduce-add for C += of K-slabs): each
+// epilogue warp stages 32 rows x 16 complex per box (SWIZZLE_128B, conflict-free) in two
+// alternating buffers and one lane issues the store, so the warps return to promoting
+// the next tile while the TMA engine drains C (thread stores of C cost a third of a
+// K = 256 step).  3 operand stages instead of 4 make room for the staging.
 struct Cfg2P {
-  static constexpr int STG_PITCH = 68;                                 // floats per staged row (32 complex + pad)
-  static constexpr int STG_BYTES = Cfg2::EPI_WARPS * 8 * STG_PITCH * 4;
-  static constexpr int SMEM = Cfg2::STAGES * Cfg2::STAGE + Cfg2::SLOTS * Cfg2::SC_BYTES + STG_BYTES + 1024 + 512;
+  static constexpr int STAGES = 3;                                     // short-K tiles: 3 operand stages
+  static constexpr int STG_WARP = 2 * 32 * 128;                        // 2 TMA-store boxes of 32 rows x 16 complex
+  static constexpr int STG_BYTES = Cfg2::EPI_WARPS * STG_WARP;         // 64 KB
+  static constexpr int STG_PITCH = 68;                                 // split-K partial path: 8 rows x 32 complex + pad
+  static constexpr int SMEM = STAGES * Cfg2::STAGE + Cfg2::SLOTS * Cfg2::SC_BYTES + STG_BYTES + 1024 + 512;
 };
 
 template <bool kTmem0>
@@ -773,8 +819,8 @@ __device__ __forceinline__ void mma_tiles_pair(uint8_t* smem, uint64_t* full, ui
     const int kc0 = split * kc_per_split;
     const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
     for (int kc = 0; kc < nk; ++kc, ++g) {
-      const int s = g % CF::STAGES;
-      const uint32_t ph = (g / CF::STAGES) & 1;
+      const int s = g % Cfg2P::STAGES;
+      const uint32_t ph = (g / Cfg2P::STAGES) & 1;
       const bool first = (kc % PROMO) == 0;
       const bool last = (kc % PROMO) == PROMO - 1 || kc == nk - 1;
       const int buf = gp & 1;
@@ -813,15 +859,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
                           const float* __restrict__ scA, const float* __restrict__ scB,
                           void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
                           int32_t nb, int32_t S, int32_t kc_per_split, float2* __restrict__ partial,
-                          int32_t accumulate, int32_t m_off, int32_t M_c) {
+                          int32_t accumulate, int32_t m_off, int32_t M_c, const __grid_constant__ CUtensorMap tmC) {
   using CF = Cfg2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* sc = reinterpret_cast<float*>(smem + CF::STAGES * CF::STAGE);   // [SLOTS][BM + BN]
-  float* stg = sc + CF::SLOTS * (BM + CF::BN);                          // [EPI_WARPS][32][STG_PITCH]
+  float* sc = reinterpret_cast<float*>(smem + Cfg2P::STAGES * CF::STAGE);   // [SLOTS][BM + BN]
+  float* stg = sc + CF::SLOTS * (BM + CF::BN);                          // [EPI_WARPS][STG_WARP bytes]
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + Cfg2P::STG_BYTES);
-  uint64_t* empty = full + CF::STAGES;
-  uint64_t* tfull = empty + CF::STAGES;
+  uint64_t* empty = full + Cfg2P::STAGES;
+  uint64_t* tfull = empty + Cfg2P::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;
   uint64_t* sempty = sfull + CF::SLOTS;
@@ -850,7 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   };
 
   if (warp == TMA_WARP && lane == 0) {
-    for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < Cfg2P::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * CF::EPI_WARPS); }
     for (int s = 0; s < CF::SLOTS; ++s) { mbar_init(&sfull[s], 1); mbar_init(&sempty[s], CF::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -889,8 +935,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
             bulk_load(d + BM, sb + (int64_t)cg * N, CF::BN * 4, &sfull[slot]);
             ++gp;
           }
-          const int s = g % CF::STAGES;
-          const uint32_t ph = (g / CF::STAGES) & 1;
+          const int s = g % Cfg2P::STAGES;
+          const uint32_t ph = (g / Cfg2P::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * CF::STAGE);
           const uint32_t fb = mapa_rank0(&full[s]);
@@ -909,7 +955,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     // ---- epilogue warps ----
     const int lg = warp & 3, ch = warp >> 2;
     const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
-    float* my_stg = stg + warp * (8 * Cfg2P::STG_PITCH);
+    float* my_stg = stg + warp * (Cfg2P::STG_WARP / 4);
+    int sb = 0;                                // TMA-store boxes issued by this warp
     int gp = 0;
     for (int tile = pair; tile < total; tile += n_pairs) {
       int b, split, m_blk, n_blk;
@@ -964,6 +1011,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
       const bool acc_c = accumulate && !partial;
       const int rbase = row0 + lg * 32, col0 = n_blk * CF::BN + ch * 64;
       const uint32_t stg_u = smem_u32(my_stg);
+      if (!partial) {
+        // 4 boxes of 32 rows x 16 complex (128-byte rows, 16-byte chunk j of row r at
+        // j ^ (r & 7): the SWIZZLE_128B layout of the C tensor map)
+        const int y = b * c_rows + c_row_off + rbase;
+#pragma unroll
+        for (int q = 0; q < 4; ++q, ++sb) {
+          const uint32_t buf = stg_u + (sb & 1) * (32 * 128);
+          if (lane == 0) bulk_wait_read1();        // the box stored from this buffer 2 rounds ago is read
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sts128(buf + lane * 128 + ((j ^ (lane & 7)) << 4),
+                   make_float4(ar[16 * q + 2 * j], ai[16 * q + 2 * j], ar[16 * q + 2 * j + 1], ai[16 * q + 2 * j + 1]));
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (acc_c) tma_reduce_add_2d(&tmC, buf, 2 * (col0 + 16 * q), y);
+            else tma_store_2d(&tmC, buf, 2 * (col0 + 16 * q), y);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
+      // split-K partials: thread stores through the staging area
       constexpr int P = Cfg2P::STG_PITCH;
 #pragma unroll
       for (int g = 0; g < 4; ++g)
@@ -993,6 +1064,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
         __syncwarp();
       }
     }
+    if (lane == 0) bulk_wait_all();              // C fully written before the CTA exits
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

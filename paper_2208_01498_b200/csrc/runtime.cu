@@ -178,6 +178,21 @@ CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int 
   return m;
 }
 
+// C of a tensor-core step, [rows][N] complex64 as [rows][2N] fp32, for TMA stores of 32 x
+// 16-complex boxes (SWIZZLE_128B)
+CUtensorMap make_c_map(void* base, int n_bits, int64_t rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cuuint64_t(2) << n_bits, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t(2) << n_bits) * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(TN_ECUDA, "cuTensorMapEncodeTiled (C) failed: " + std::to_string((int)r));
+  return m;
+}
+
 template <int BN>
 void ensure_gemm_attr() {
   static bool done = false;
@@ -212,6 +227,7 @@ struct TcStep {
   int m_lo = 0;                   // log2 rows of X per row slab (= m_bits without row slabs)
   int n_mslabs = 1;               // row slabs of X (bounded pack buffer when C is large)
   CUtensorMap ta, tb;
+  CUtensorMap tc;                 // C [b * M_c + row][N] complex64 for TMA stores (pair kernels)
   double flops;
 };
 
@@ -248,6 +264,12 @@ bool gemm_persist_enabled() {
     return !(e && e[0] == '0');
   }();
   return v;
+}
+
+// the persistent pair kernel serves steps with <= 32 K stages per tile
+bool uses_persist(const TcStep& t) {
+  const int64_t stages_per_tile = std::min<int64_t>(t.kc_split, ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK);
+  return t.kind == K_TC && t.pair && gemm_persist_enabled() && stages_per_tile <= 32;
 }
 
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
@@ -376,8 +398,7 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
     const int m_off = ms << t.m_lo;
     // persistent tile loop only for short K per tile (<= 32 stages): there the per-CTA
     // prologue / fill / drain is a large share; long tiles are faster one per CTA pair
-    const int64_t stages_per_tile = std::min<int64_t>(t.kc_split, ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK);
-    if (t.pair && gemm_persist_enabled() && stages_per_tile <= 32) {
+    if (uses_persist(t)) {
       static bool attr2p = false;
       if (!attr2p) {
         CK(cudaFuncSetAttribute(tnd::tc::cgemm2p_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -388,7 +409,7 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
       const int64_t n_pairs = std::min<int64_t>(tiles, 74);
       tnd::tc::cgemm2p_f16x2s_kernel<<<(unsigned)(2 * n_pairs), tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2P::SMEM, st>>>(
           t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.S,
-          t.kc_split, partial, acc, m_off, 1 << t.m_bits);
+          t.kc_split, partial, acc, m_off, 1 << t.m_bits, t.tc);
     } else if (t.pair) {
       static bool attr2 = false;
       if (!attr2) {
@@ -400,7 +421,7 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
       dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
       tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
           t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
-          t.kc_split, partial, acc, m_off, 1 << t.m_bits);
+          t.kc_split, partial, acc, m_off, 1 << t.m_bits, t.tc);
     } else if (t.BN == 128) {
       ensure_gemm_attr<128>();
       tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
@@ -1143,6 +1164,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     if (t.kind != K_TC) continue;
     t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
     t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
+    if (t.pair)
+      t.tc = make_c_map(P.arena + P.node_off[t.c_node], t.n_bits, int64_t(1) << (t.nb_bits + t.m_bits));
   }
 
   // ---- uploads ----
@@ -1238,6 +1261,8 @@ void add_lane(tn_plan_s& P) {
     if (t.kind != K_TC) continue;
     t.ta = make_plane_map(l.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
     t.tb = make_plane_map(l.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
+    if (t.pair)
+      t.tc = make_c_map(l.arena + P.node_off[t.c_node], t.n_bits, int64_t(1) << (t.nb_bits + t.m_bits));
   }
   CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
   cudaGraph_t g;
@@ -1784,6 +1809,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       if (t.kind == K_TC) {
         t.ta = make_plane_map(scratch + t.x_off, t.k_lo, t.m_lo, nb, 128, 4);
         t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
+        if (t.pair) t.tc = make_c_map(C, my, int64_t(1) << (nb + mx));
       }
       launch_tc(t, scratch, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));  // host staging buffers must outlive the copies
