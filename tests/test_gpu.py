@@ -260,15 +260,17 @@ def test_pair_complex128_dmma_path(case):
 
 
 def test_pair_tensor_core_k_slabs(monkeypatch):
-    """K-slab packing (bounded pack buffers): forced by lowering the pack cap in a child
-    process (the cap is read once per process)."""
+    """K-slab packing (bounded pack buffers): forced by lowering the pack cap in child
+    processes (the cap is read once per process).  Cap 2^13: K-slabs and row slabs of
+    single-CTA and pair steps, incl. (0, 9, 8, 10): 32 K-slabs on the persistent pair
+    kernel, C += by TMA reduce-add; cap 2^23: (0, 12, 11, 14), 8 K-slabs of 64 stages on
+    the one-tile-per-pair kernel, 512 CTAs (no split-K), reduce-add from its epilogue."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import sys; sys.path.insert(0, '.')
         sys.path.insert(0, 'tests')
         import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
-        # K-slabs, then row slabs of X (X over the cap, Y under it), with batch and permutations
-        for case in [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2), (0, 10, 7, 4, None), (1, 10, 7, 4, 3), (0, 11, 8, 4, 5)]:
+        for case in CASES:
             nb, m, n, k, ps = case
             ia, ib, ic, dims = T._gemm_case(nb, m, n, k, ps)
             got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=31)
@@ -276,10 +278,14 @@ def test_pair_tensor_core_k_slabs(monkeypatch):
             assert np.all(err <= T.c64_tol(2 ** k) * bound + 1e-30), (case, (err / bound).max())
         print('ok')
     """)
-    env = dict(os.environ, TN_PACK_CAP_LOG2="13")
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for cap, cases in (("13", [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2), (0, 10, 7, 4, None), (1, 10, 7, 4, 3),
+                               (0, 11, 8, 4, 5), (0, 9, 8, 10, None)]),
+                       ("23", [(0, 12, 11, 14, None)])):
+        env = dict(os.environ, TN_PACK_CAP_LOG2=cap)
+        r = subprocess.run([sys.executable, "-c", code.replace("CASES", repr(cases))], capture_output=True,
+                           text=True, env=env, cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_plan_with_bounded_pack_buffers():
