@@ -268,8 +268,12 @@ bool gemm_persist_enabled() {
 
 // the persistent pair kernel serves steps with <= 32 K stages per tile
 bool uses_persist(const TcStep& t) {
+  static const int64_t max_stages = [] {       // TN_PERSIST_MAX_STAGES: experiments
+    const char* e = std::getenv("TN_PERSIST_MAX_STAGES");
+    return e ? (int64_t)std::atoll(e) : int64_t(32);
+  }();
   const int64_t stages_per_tile = std::min<int64_t>(t.kc_split, ((int64_t(1) << t.k_lo) + tnd::tc::BK - 1) / tnd::tc::BK);
-  return t.kind == K_TC && t.pair && gemm_persist_enabled() && stages_per_tile <= 32;
+  return t.kind == K_TC && t.pair && gemm_persist_enabled() && stages_per_tile <= max_stages;
 }
 
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
