@@ -196,54 +196,109 @@ __global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_
 }
 
 // ------------------------------------------------------------------- wide ----
-// C[b][m][n] = sum_k X[b][m][k] Y[b][n][k] with K <= WD_MAXK (16): a CTA writes a tile of
-// WD_TM rows x WD_TN columns (consecutive threads on consecutive n: coalesced stores),
-// with the X rows and the Y columns of the tile staged in shared memory (Y transposed
-// to [k][n] so the per-thread reads are conflict-free).  Tiles are visited
-// grid-stride; batch b, row tile and column tile are flattened into one tile index.
-constexpr int WD_THREADS = 256, WD_TM = 32, WD_TN = 128, WD_MAXK = 16;
+// C[b][m][n] = sum_k X[b][m][k] Y[b][n][k] with K <= WD_MAXK (16): a short contraction
+// onto a large output, bound by writing C.  A CTA covers rows [m0, m0 + tm) (tm <=
+// WD_TM) x columns [n0, n0 + 256): the X rows go to shared memory (fp64, read as
+// broadcasts), each thread keeps its column's Y row in registers (K contiguous in the
+// planar operand: vector loads) and writes its column of the tile, consecutive threads on
+// consecutive n (coalesced).  Tiles are visited grid-stride with the row tile fastest so
+// CTAs running together share Y columns in L2.  Accumulation in the plan's type: fp32 FMA
+// for complex64 (K <= 16 terms: the fp32-path bound of DESIGN.md "Tolerances"; fp64 here
+// ran at the FP64 pipe's ~12 TFLOP/s, 4x slower than writing C), fp64 for complex128.
+constexpr int WD_THREADS = 256, WD_TM = 32, WD_MAXK = 16;
 
-template <typename R>
+template <typename R, int CPT>
 __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ X, const R* __restrict__ Y,
                                                           void* const* __restrict__ ptrs, int32_t c_node,
                                                           int32_t m_bits, int32_t n_bits, int32_t k_bits,
                                                           int64_t n_tiles) {
+  // CPT adjacent columns per thread (2 for complex64: each broadcast X load serves two
+  // outputs and each thread stores 16 bytes)
   using C2 = typename cplx_t<R>::type;
-  __shared__ double xs[2][WD_TM][WD_MAXK];       // fp64: each element converted once per tile
-  __shared__ double ys[2][WD_MAXK][WD_TN];
+  __shared__ __align__(16) R xs[2][WD_TM][WD_MAXK];
   C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
   const int64_t M = int64_t(1) << m_bits, N = int64_t(1) << n_bits;
   const int K = 1 << k_bits;
-  const int tm = (int)(M < WD_TM ? M : WD_TM), tn = (int)(N < WD_TN ? N : WD_TN);
-  const int64_t mt = M / tm, nt = N / tn;
+  const int tm = (int)(M < WD_TM ? M : WD_TM);
+  constexpr int TN = WD_THREADS * CPT;
+  const int64_t mt = M / tm, ncb = (N + TN - 1) / TN;
+  constexpr int V = 16 / sizeof(R);                  // elements per 16-byte vector load
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t b = tile / (mt * nt), r = tile % (mt * nt);
-    const int64_t m0 = (r / nt) * tm, n0 = (r % nt) * tn;
+    const int64_t b = tile / (ncb * mt), r = tile % (ncb * mt);
+    const int64_t m0 = (r % mt) * tm, n = (r / mt) * TN + threadIdx.x * CPT;
     const R* __restrict__ xb = X + b * 2 * M * K;
     const R* __restrict__ yb = Y + b * 2 * N * K;
-    __syncthreads();
+    __syncthreads();                                 // the previous tile's xs reads are done
     for (int e = threadIdx.x; e < 2 * tm * K; e += WD_THREADS) {
       const int p = e / (tm * K), i = (e / K) % tm, k = e % K;
       xs[p][i][k] = xb[(p * M + m0 + i) * K + k];
     }
-    for (int e = threadIdx.x; e < 2 * tn * K; e += WD_THREADS) {
-      const int p = e / (tn * K), j = (e / K) % tn, k = e % K;
-      ys[p][k][j] = yb[(p * N + n0 + j) * K + k];
-    }
     __syncthreads();
-    // threads: column j = tid % tn, row group rg = tid / tn (WD_THREADS / tn groups)
-    const int j = threadIdx.x % tn, groups = WD_THREADS / tn, rg = threadIdx.x / tn;
-    if (rg >= groups) continue;
-    for (int i = rg; i < tm; i += groups) {
-      double re = 0.0, im = 0.0;
-      for (int k = 0; k < K; ++k) {
-        const double ar = xs[0][i][k], ai = xs[1][i][k], br = ys[0][k][j], bi = ys[1][k][j];
-        re = fma(ar, br, re);
-        re = fma(-ai, bi, re);
-        im = fma(ar, bi, im);
-        im = fma(ai, br, im);
+    if (n >= N) continue;
+    R yr[CPT][WD_MAXK], yi[CPT][WD_MAXK];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (K % V == 0) {
+#pragma unroll
+        for (int q = 0; q < WD_MAXK / V; ++q) {
+          if (q * V < K) {
+            R vr[V], vi[V];
+            *reinterpret_cast<float4*>(vr) = __ldg(reinterpret_cast<const float4*>(yb + (n + c) * K) + q);
+            *reinterpret_cast<float4*>(vi) = __ldg(reinterpret_cast<const float4*>(yb + (N + n + c) * K) + q);
+#pragma unroll
+            for (int u = 0; u < V; ++u) { yr[c][q * V + u] = vr[u]; yi[c][q * V + u] = vi[u]; }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < WD_MAXK; ++k)
+          if (k < K) { yr[c][k] = __ldg(yb + (n + c) * K + k); yi[c][k] = __ldg(yb + (N + n + c) * K + k); }
       }
-      C[(b * M + m0 + i) * N + n0 + j] = C2{(R)re, (R)im};
+    }
+    C2* __restrict__ cp = C + (b * M + m0) * N + n;
+    for (int i = 0; i < tm; ++i) {
+      R re[CPT], im[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) { re[c] = 0; im[c] = 0; }
+      if (K % V == 0) {       // the row of X as 16-byte broadcast loads (the LDS count bounded this loop)
+#pragma unroll
+        for (int q = 0; q < WD_MAXK / V; ++q) {
+          if (q * V < K) {
+            R xr[V], xi[V];
+            *reinterpret_cast<float4*>(xr) = *reinterpret_cast<const float4*>(&xs[0][i][q * V]);
+            *reinterpret_cast<float4*>(xi) = *reinterpret_cast<const float4*>(&xs[1][i][q * V]);
+#pragma unroll
+            for (int u = 0; u < V; ++u)
+#pragma unroll
+              for (int c = 0; c < CPT; ++c) {
+                re[c] = fma(xr[u], yr[c][q * V + u], re[c]);
+                re[c] = fma(-xi[u], yi[c][q * V + u], re[c]);
+                im[c] = fma(xr[u], yi[c][q * V + u], im[c]);
+                im[c] = fma(xi[u], yr[c][q * V + u], im[c]);
+              }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < WD_MAXK; ++k) {
+          if (k < K) {
+            const R ar = xs[0][i][k], ai = xs[1][i][k];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              re[c] = fma(ar, yr[c][k], re[c]);
+              re[c] = fma(-ai, yi[c][k], re[c]);
+              im[c] = fma(ar, yi[c][k], im[c]);
+              im[c] = fma(ai, yr[c][k], im[c]);
+            }
+          }
+        }
+      }
+      if constexpr (CPT == 2) {
+        static_assert(sizeof(R) == 4, "two columns per thread: complex64 only");
+        *reinterpret_cast<float4*>(cp + (int64_t)i * N) = make_float4(re[0], im[0], re[1], im[1]);
+      } else {
+        cp[(int64_t)i * N] = C2{re[0], im[0]};
+      }
     }
   }
 }

@@ -353,10 +353,19 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
           partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
       g_launches++;
     } else {
-      const int64_t tm = std::min(tnd::WD_TM, 1 << t.m_bits), tn = std::min(tnd::WD_TN, 1 << t.n_bits);
-      const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits)) / (tm * tn);
-      tnd::wide_kernel<R><<<(unsigned)std::min<int64_t>(tiles, 148 * 8), tnd::WD_THREADS, 0, st>>>(
-          X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles);
+      // complex64 with N >= 2: two adjacent columns per thread
+      const bool two = sizeof(R) == 4 && t.n_bits >= 1;
+      const int64_t tm = std::min(tnd::WD_TM, 1 << t.m_bits), tn = int64_t(tnd::WD_THREADS) * (two ? 2 : 1);
+      const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits)) / tm * (((int64_t(1) << t.n_bits) + tn - 1) / tn);
+      const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
+      if constexpr (sizeof(R) == 4) {
+        if (two)
+          tnd::wide_kernel<R, 2><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits,
+                                                                    t.k_bits, tiles);
+      }
+      if (!two)
+        tnd::wide_kernel<R, 1><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits,
+                                                                  t.k_bits, tiles);
       g_launches++;
     }
   }
