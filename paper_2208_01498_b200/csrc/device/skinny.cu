@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_planar_kernel(const void
 // cut into groups of GM x GN <= 16 (GM = min(M, 4) rows of X, GN = min(N, 16 / GM) rows
 // of Y).  CTA (s, b) covers K range [s kc, (s + 1) kc); each of its 8 warps takes one
 // group (several warps per group interleave the range) and streams the group's rows
-// straight from HBM, lanes on consecutive k (coalesced 128-byte row segments, no shared
-// memory, no barriers), accumulating GM GN complex fp64 sums per lane.  Warp sums go to
+// straight from HBM, lanes on consecutive k (coalesced row segments, no shared memory,
+// no barriers), accumulating GM GN complex fp64 sums per lane (complex64: fp32 blocks of
+// 8 k per lane folded into the fp64 sums).  Warp sums go to
 // partial[b][s * WS + w][o] (WS warps per group), summed in order by
 // skinny_reduce_kernel -- deterministic.
 constexpr int SK_THREADS = 256, SK_WARPS = SK_THREADS / 32;
@@ -126,21 +127,72 @@ __global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict_
     const R* xi_p = xb + (int64_t)(M + m0) * K;
     const R* yr_p = yb + (int64_t)n0 * K;
     const R* yi_p = yb + (int64_t)(N + n0) * K;
-    for (int64_t k = k_begin + wsub * 32 + lane; k < k_end; k += 32 * ws) {
-      double xr[GM], xi[GM], yr[GN], yi[GN];
-#pragma unroll
-      for (int i = 0; i < GM; ++i) { xr[i] = xr_p[(int64_t)i * K + k]; xi[i] = xi_p[(int64_t)i * K + k]; }
-#pragma unroll
-      for (int j = 0; j < GN; ++j) { yr[j] = yr_p[(int64_t)j * K + k]; yi[j] = yi_p[(int64_t)j * K + k]; }
+    if constexpr (sizeof(R) == 4) {
+      // complex64: each lane takes 4 consecutive k (16-byte loads, 512-byte warp segments);
+      // products accumulate in fp32 over blocks of 8 k per lane, each block then added to
+      // the fp64 sums (the FP64 pipe bounded the all-fp64 loop at ~1 TB/s)
+      float br[GM][GN], bi[GM][GN];
 #pragma unroll
       for (int i = 0; i < GM; ++i)
 #pragma unroll
-        for (int j = 0; j < GN; ++j) {
-          ar[i][j] = fma(xr[i], yr[j], ar[i][j]);
-          ar[i][j] = fma(-xi[i], yi[j], ar[i][j]);
-          ai[i][j] = fma(xr[i], yi[j], ai[i][j]);
-          ai[i][j] = fma(xi[i], yr[j], ai[i][j]);
+        for (int j = 0; j < GN; ++j) { br[i][j] = 0.f; bi[i][j] = 0.f; }
+      int cnt = 0;
+      for (int64_t k = k_begin + (int64_t)(wsub * 32 + lane) * 4; k < k_end; k += 128 * ws) {
+        float4 xr[GM], xi[GM], yr[GN], yi[GN];
+#pragma unroll
+        for (int i = 0; i < GM; ++i) {
+          xr[i] = __ldg(reinterpret_cast<const float4*>(xr_p + (int64_t)i * K + k));
+          xi[i] = __ldg(reinterpret_cast<const float4*>(xi_p + (int64_t)i * K + k));
         }
+#pragma unroll
+        for (int j = 0; j < GN; ++j) {
+          yr[j] = __ldg(reinterpret_cast<const float4*>(yr_p + (int64_t)j * K + k));
+          yi[j] = __ldg(reinterpret_cast<const float4*>(yi_p + (int64_t)j * K + k));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int i = 0; i < GM; ++i)
+#pragma unroll
+            for (int j = 0; j < GN; ++j) {
+              const float a_r = (&xr[i].x)[u], a_i = (&xi[i].x)[u], b_r = (&yr[j].x)[u], b_i = (&yi[j].x)[u];
+              br[i][j] = fmaf(a_r, b_r, br[i][j]);
+              br[i][j] = fmaf(-a_i, b_i, br[i][j]);
+              bi[i][j] = fmaf(a_r, b_i, bi[i][j]);
+              bi[i][j] = fmaf(a_i, b_r, bi[i][j]);
+            }
+        if (++cnt == 2) {
+          cnt = 0;
+#pragma unroll
+          for (int i = 0; i < GM; ++i)
+#pragma unroll
+            for (int j = 0; j < GN; ++j) {
+              ar[i][j] += (double)br[i][j]; ai[i][j] += (double)bi[i][j];
+              br[i][j] = 0.f; bi[i][j] = 0.f;
+            }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int j = 0; j < GN; ++j) { ar[i][j] += (double)br[i][j]; ai[i][j] += (double)bi[i][j]; }
+    } else {
+      for (int64_t k = k_begin + wsub * 32 + lane; k < k_end; k += 32 * ws) {
+        double xr[GM], xi[GM], yr[GN], yi[GN];
+#pragma unroll
+        for (int i = 0; i < GM; ++i) { xr[i] = xr_p[(int64_t)i * K + k]; xi[i] = xi_p[(int64_t)i * K + k]; }
+#pragma unroll
+        for (int j = 0; j < GN; ++j) { yr[j] = yr_p[(int64_t)j * K + k]; yi[j] = yi_p[(int64_t)j * K + k]; }
+#pragma unroll
+        for (int i = 0; i < GM; ++i)
+#pragma unroll
+          for (int j = 0; j < GN; ++j) {
+            ar[i][j] = fma(xr[i], yr[j], ar[i][j]);
+            ar[i][j] = fma(-xi[i], yi[j], ar[i][j]);
+            ai[i][j] = fma(xr[i], yi[j], ai[i][j]);
+            ai[i][j] = fma(xi[i], yr[j], ai[i][j]);
+          }
+      }
     }
 #pragma unroll
     for (int i = 0; i < GM; ++i)

@@ -332,7 +332,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
                                              t.k_bits) : "");
     if (t.kind == K_SKINNY) {
       const int64_t K = int64_t(1) << t.k_lo;
-      const int64_t kc = (K + t.S - 1) / t.S;
+      const int64_t kc = ((K + t.S - 1) / t.S + 127) / 128 * 128;   // 16-byte aligned K ranges
       double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
       int gm, gn, ng, ws;
       tnd::skinny_groups(t.m_bits, t.n_bits, gm, gn, ng, ws);
