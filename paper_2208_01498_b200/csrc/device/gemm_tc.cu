@@ -79,7 +79,7 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 // [b][K / 64][r] fp32 (one per row and 64-element K chunk; one per row if K < 64).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
 // inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
-__global__ void __launch_bounds__(PACK_THREADS, 3) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
                                                                    int64_t src_base) {
