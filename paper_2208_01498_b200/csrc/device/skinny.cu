@@ -16,7 +16,7 @@ namespace tnd {
 // Output planes [b][2][rows][K] of R: (re plane, im plane); the host built tile_dst /
 // q_hi for 2 planes per batch (see PackDesc).
 template <typename R>
-__global__ void __launch_bounds__(PACK_THREADS, 3) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
+__global__ void __launch_bounds__(PACK_THREADS, sizeof(R) == 4 ? 4 : 3) pack_planar_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    R* __restrict__ out, int64_t src_base) {
   using C2 = typename cplx_t<R>::type;
