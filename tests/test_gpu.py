@@ -120,6 +120,7 @@ TC_CASES = [
     (0, 8, 7, 4, None),       # one pair tile, K = 16
     (2, 8, 7, 10, 3),         # batch 4, permuted, 32 stages
     (0, 9, 9, 14, 11),        # 2 x 4 pair tiles, split-K over 4 splits, permuted
+    (0, 12, 11, 11, 4),       # 256 pair tiles (no split), 64 stages: one tile per pair, TMA-store epilogue
 ]
 
 
