@@ -274,10 +274,13 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
   const int tm = (int)(M < WD_TM ? M : WD_TM);
   constexpr int TN = WD_THREADS * CPT;
   const int64_t mt = M / tm, ncb = (N + TN - 1) / TN;
+  // N < TN: the threads split into row groups, each covering all N columns
+  const int tpr = (int)((N < TN ? N : TN) / CPT);   // threads per row group
+  const int groups = WD_THREADS / tpr, rg = threadIdx.x / tpr;
   constexpr int V = 16 / sizeof(R);                  // elements per 16-byte vector load
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t b = tile / (ncb * mt), r = tile % (ncb * mt);
-    const int64_t m0 = (r % mt) * tm, n = (r / mt) * TN + threadIdx.x * CPT;
+    const int64_t m0 = (r % mt) * tm, n = (r / mt) * TN + (threadIdx.x % tpr) * CPT;
     const R* __restrict__ xb = X + b * 2 * M * K;
     const R* __restrict__ yb = Y + b * 2 * N * K;
     __syncthreads();                                 // the previous tile's xs reads are done
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
       xs[p][i][k] = xb[(p * M + m0 + i) * K + k];
     }
     __syncthreads();
-    if (n >= N) continue;
+    if (n >= N || rg >= groups) continue;
     R yr[CPT][WD_MAXK], yi[CPT][WD_MAXK];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
       }
     }
     C2* __restrict__ cp = C + (b * M + m0) * N + n;
-    for (int i = 0; i < tm; ++i) {
+    for (int i = rg; i < tm; i += groups) {
       R re[CPT], im[CPT];
 #pragma unroll
       for (int c = 0; c < CPT; ++c) { re[c] = 0; im[c] = 0; }
