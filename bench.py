@@ -407,13 +407,13 @@ def run_ours(args):
         if dtype == tb.TN_C64:
             # DRAM traffic (bytes) of one launch of the bench's dominant GEMM shape from the
             # committed ncu --set full capture: a K-slab of the (18, 12, 16) steps (64% of a
-            # configs[1] step).  A is re-read ~8x from DRAM (L2 hit 74%), harmless for a
+            # configs[1] step).  A is re-read ~6x from DRAM (L2 hit 79%), harmless for a
             # tensor-bound kernel (DRAM at 13%)
-            roof["traffic"] = 6.935e10 + 8.796e9
+            roof["traffic"] = 5.715e10 + 8.663e9
             roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[2^18][2^12] = A[2^18][2^12] B[2^12][2^12] "
                                                "(one K-slab of the configs[1] (18, 12, 16) steps)",
-                                     "dram_bytes": 6.935e10 + 8.796e9, "algorithmic_bytes": 1.731e10,
-                                     "tensor_active": 0.931, "source": "profiles/r01/ncu_full_summary.md"}
+                                     "dram_bytes": 5.715e10 + 8.663e9, "algorithmic_bytes": 1.731e10,
+                                     "tensor_active": 0.930, "source": "profiles/r01/ncu_full_summary.md"}
     else:
         roof = {"bound": "hbm", "achieved": small_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
