@@ -170,6 +170,10 @@ constexpr int PROMO = 2;   // stages per TMEM accumulation = one 64-element scal
 // single-CTA kernel 8.
 constexpr int GROUP_M = 8, GROUP_M_PAIR = 4, GROUP_M_PERSIST = 32;
 __device__ int d_group_m = 0;   // > 0: TN_GEMM_GROUP_M override (raster experiments)
+// pair kernel: odd raster groups sweep the N tiles backwards, so the B panels the last
+// wave read are still in L2 when the next group starts (DRAM reads 57 -> 51 GB on the
+// bench's dominant slab, ~1% faster); TN_GEMM_SERP=0 turns it off
+__device__ int d_serp = 1;
 
 template <int BN>
 struct Cfg {
@@ -712,7 +716,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   const int first_m = group * group_m;
   const int gm = min(n_tiles_m - first_m, group_m);
   const int m_blk = first_m + (pid % (group_m * n_tiles_n)) % gm;
-  const int n_blk = (pid % (group_m * n_tiles_n)) / gm;
+  const int n_fwd = (pid % (group_m * n_tiles_n)) / gm;
+  const int n_blk = (d_serp && (group & 1)) ? n_tiles_n - 1 - n_fwd : n_fwd;
   const int row0 = m_blk * 256 + (int)rank * BM;
   const int b = blockIdx.z % nb, split = blockIdx.z / nb;
   const int nk_all = (K + BK - 1) / BK;

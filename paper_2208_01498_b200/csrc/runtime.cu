@@ -380,6 +380,11 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
       const int g = std::atoi(e);
       CK(cudaMemcpyToSymbol(tnd::tc::d_group_m, &g, sizeof(int)));
     }
+    const char* sp = std::getenv("TN_GEMM_SERP");
+    if (sp) {
+      const int v = std::atoi(sp);
+      CK(cudaMemcpyToSymbol(tnd::tc::d_serp, &v, sizeof(int)));
+    }
     return true;
   }();
   (void)group_set;
