@@ -692,7 +692,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
                          const float* __restrict__ scA, const float* __restrict__ scB,
                          void* const* __restrict__ ptrs, int32_t c_node, int32_t M, int32_t N, int32_t K,
                          int32_t nb, int32_t kc_per_split, float2* __restrict__ partial, int32_t accumulate,
-                         int32_t m_off, int32_t M_c, const __grid_constant__ CUtensorMap tmC) {
+                         int32_t m_off, int32_t M_c, const __grid_constant__ CUtensorMap tmC, int32_t k_base) {
   using CF = Cfg2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -721,7 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   const int row0 = m_blk * 256 + (int)rank * BM;
   const int b = blockIdx.z % nb, split = blockIdx.z / nb;
   const int nk_all = (K + BK - 1) / BK;
-  const int kc0 = split * kc_per_split;
+  const int kc0 = k_base + split * kc_per_split;     // k_base: K-chunk of a long-K step (stages)
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
   const int nch_all = (nk_all + PROMO - 1) / PROMO;
   const int n_promo = (nk + PROMO - 1) / PROMO;

@@ -226,6 +226,7 @@ struct TcStep {
   int kc_split = 1 << 30;         // K stages per split (K_TC)
   int m_lo = 0;                   // log2 rows of X per row slab (= m_bits without row slabs)
   int n_mslabs = 1;               // row slabs of X (bounded pack buffer when C is large)
+  int n_kchunks = 1;              // pair kernel launches over consecutive K ranges of kc_split stages
   CUtensorMap ta, tb;
   CUtensorMap tc;                 // C [b * M_c + row][N] complex64 for TMA stores (pair kernels)
   double flops;
@@ -437,9 +438,12 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
       }
       const int64_t pairs = (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7));
       dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
-      tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
-          t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
-          t.kc_split, partial, acc, m_off, 1 << t.m_bits, t.tc);
+      for (int ch = 0; ch < t.n_kchunks; ++ch) {
+        tnd::tc::cgemm2_f16x2s_kernel<<<grid2, tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2::SMEM, st>>>(
+            t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits,
+            t.kc_split, partial, acc || ch > 0, m_off, 1 << t.m_bits, t.tc, ch * t.kc_split);
+        if (ch > 0) g_launches++;
+      }
     } else if (t.BN == 128) {
       ensure_gemm_attr<128>();
       tnd::tc::cgemm_f16x2s_kernel<128><<<grid, tnd::tc::Cfg<128>::THREADS, tnd::tc::Cfg<128>::SMEM, st>>>(
@@ -534,6 +538,21 @@ void finish_tc_shape(TcStep& t) {
   kc = (kc + tnd::tc::PROMO - 1) / tnd::tc::PROMO * tnd::tc::PROMO;   // splits start on a scale chunk
   t.kc_split = (int)kc;
   t.S = (int)((nk_all + kc - 1) / kc);
+  // K-chunks: a long-K pair GEMM runs as consecutive launches over K ranges of 16384
+  // (8192 when K = 16384), C += by TMA reduce-add -- the waves of a launch then share the
+  // operand panels of one K range in L2: DRAM reads 101 -> 71 GB and 1.31 -> 1.36 GHz under
+  // the power cap on a (2^14, 2^12, 2^16) step (scripts/kslab_probe.sh); TN_GEMM_KCHUNK=0
+  // turns it off
+  static const bool kchunk = [] {
+    const char* e = std::getenv("TN_GEMM_KCHUNK");
+    return !(e && e[0] == '0');
+  }();
+  t.n_kchunks = 1;
+  if (kchunk && t.pair && t.S == 1 && nk_all >= 512) {
+    const int64_t cs = nk_all >= 1024 ? 512 : 256;
+    t.kc_split = (int)cs;
+    t.n_kchunks = (int)((nk_all + cs - 1) / cs);
+  }
 }
 int64_t tc_partial_bytes(const TcStep& t) {
   if (t.kind == K_SKINNY) return (int64_t(16) * t.S * skinny_ws(t)) << (t.nb_bits + t.m_bits + t.n_bits);

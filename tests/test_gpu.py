@@ -121,6 +121,7 @@ TC_CASES = [
     (2, 8, 7, 10, 3),         # batch 4, permuted, 32 stages
     (0, 9, 9, 14, 11),        # 2 x 4 pair tiles, split-K over 4 splits, permuted
     (0, 12, 11, 11, 4),       # 256 pair tiles (no split), 64 stages: one tile per pair, TMA-store epilogue
+    (0, 12, 11, 14, None),    # K = 16384: two K-chunk launches of 8192, C += by TMA reduce-add
 ]
 
 
