@@ -215,8 +215,10 @@ int tn_plan_set_lanes(tn_plan plan, int32_t n_lanes);
  * row-major over their index lists; dims[i] is the dimension of index id i
  * (0 <= i < n_dims, powers of two).  path: TN_PATH_AUTO picks the kernel like a
  * plan does; TN_PATH_SMALL / TC / SKINNY / WIDE force one (TN_EUNSUPPORTED if the
- * shape is outside what that kernel handles).
- * Asynchronous on `stream`; scratch memory is taken from an internal pool.
+ * shape is outside what that kernel handles).  C must be 16-byte aligned (the
+ * tensor-core pair kernels store it by TMA, the wide kernel by 16-byte vectors).
+ * Runs on `stream` and synchronizes it before returning (its scratch buffers, taken
+ * from the stream-ordered pool, are freed).
  */
 int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t* inds_a,
                      const void* B, int32_t rank_b, const int32_t* inds_b, void* C,
