@@ -16,10 +16,10 @@ namespace tnd {
 
 // ------------------------------------------------------------------ DMMA -----
 namespace zg {
-constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256, STAGES = 2;
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256, STAGES = 3;
 constexpr int PLANE_TILE = BM * BK;                       // doubles per plane per tile (BM == BN)
 constexpr int STAGE_DOUBLES = 4 * PLANE_TILE;             // A re, A im, B re, B im
-constexpr int SMEM = STAGES * STAGE_DOUBLES * 8;          // 64 KB
+constexpr int SMEM = STAGES * STAGE_DOUBLES * 8;          // 96 KB (2 CTAs per SM)
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ int swz(int row, int col) {      // col in doubles (0..15)
@@ -84,16 +84,19 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __
       for (int r = 0; r < 4; ++r) { cr[i][j][r] = 0.0; ci[i][j][r] = 0.0; }
 
   const int nk = (K + BK - 1) / BK;
-  load_stage(0, 0);
+  // STAGES-deep cp.async ring: stages kc + 1 .. kc + STAGES - 1 are in flight while stage
+  // kc is consumed (one commit group per stage, empty groups past the end keep the count)
+#pragma unroll
+  for (int p = 0; p < STAGES - 1; ++p) {
+    if (p < nk) load_stage(p, p * BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int kc = 0; kc < nk; ++kc) {
-    if (kc + 1 < nk) {
-      load_stage((kc + 1) & 1, (kc + 1) * BK);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
     __syncthreads();
-    const double* st = sm + (kc & 1) * STAGE_DOUBLES;
+    if (kc + STAGES - 1 < nk) load_stage((kc + STAGES - 1) % STAGES, (kc + STAGES - 1) * BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* st = sm + (kc % STAGES) * STAGE_DOUBLES;
     const double* sAr = st;
     const double* sAi = st + PLANE_TILE;
     const double* sBr = st + 2 * PLANE_TILE;
@@ -127,7 +130,6 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __
           dmma(ci[i][j], ai[i][0], ai[i][1], br[j]);
         }
     }
-    __syncthreads();
   }
   double2* C = reinterpret_cast<double2*>(ptrs[c_node]) + (int64_t)b * M * (int64_t)N;
 #pragma unroll
