@@ -95,11 +95,22 @@ class Clocks:
             if self.stop.wait(self.period):
                 return
 
+    def _handle(self, nv):
+        # the CUDA device's own NVML handle by PCI address (NVML enumerates every GPU of the
+        # machine regardless of CUDA_VISIBLE_DEVICES), else by index
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
     def __enter__(self):
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            h = self._handle(nv)
             first = threading.Event()
             self.t = threading.Thread(target=self._poll, args=(nv, h, first), daemon=True)
             self.t.start()
