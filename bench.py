@@ -78,7 +78,8 @@ class Clocks:
     def __init__(self, index=0, period_s=0.005):
         self.index = index
         self.period = period_s
-        self.rows = []                  # (sm_mhz, max_mhz, reasons bitmask)
+        self.rows = []                  # (sm_mhz, max_mhz, reasons bitmask[, board power W])
+        self.limit_w = None
         self.proc = None
         self.stop = threading.Event()
         self.t = None
@@ -88,7 +89,10 @@ class Clocks:
             try:
                 self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
                                   float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
-                                  int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                                  int(nv.nvmlDeviceGetCurrentClocksEventReasons(h)),
+                                  nv.nvmlDeviceGetPowerUsage(h) / 1000.0))
+                if self.limit_w is None:
+                    self.limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
             except Exception:
                 pass
             first.set()
@@ -152,8 +156,13 @@ class Clocks:
         rows = list(self.rows)
         sm = [r[0] for r in rows]
         reasons = sorted({n for r in rows for n, m in zip(self.NAMES, self.MASKS) if r[2] & m})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(r[1] for r in rows) if rows else None,
-                "reasons": reasons, "samples": len(rows), "sampler": "nvml" if self.t is not None else "nvidia-smi"}
+        pw = [r[3] for r in rows if len(r) > 3]
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(r[1] for r in rows) if rows else None,
+               "reasons": reasons, "samples": len(rows), "sampler": "nvml" if self.t is not None else "nvidia-smi"}
+        if pw:
+            out["power_w"] = float(np.median(pw))
+            out["power_limit_w"] = self.limit_w
+        return out
 
 
 def dist_env():
