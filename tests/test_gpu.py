@@ -269,7 +269,9 @@ def test_pair_tensor_core_k_slabs(monkeypatch):
     processes (the cap is read once per process).  Cap 2^13: K-slabs and row slabs of
     single-CTA and pair steps, incl. (0, 9, 8, 10): 32 K-slabs on the persistent pair
     kernel, C += by TMA reduce-add; cap 2^23: (0, 12, 11, 14), 8 K-slabs of 64 stages on
-    the one-tile-per-pair kernel, 512 CTAs (no split-K), reduce-add from its epilogue."""
+    the one-tile-per-pair kernel, 512 CTAs (no split-K), reduce-add from its epilogue;
+    with a batch index and permuted layouts: cap 2^21 (1, 11, 10, 12) on the persistent
+    kernel, cap 2^24 (1, 12, 11, 13) on the one-tile-per-pair kernel."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import sys; sys.path.insert(0, '.')
@@ -286,7 +288,9 @@ def test_pair_tensor_core_k_slabs(monkeypatch):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for cap, cases in (("13", [(0, 7, 7, 9, 1), (1, 6, 7, 14, 2), (0, 10, 7, 4, None), (1, 10, 7, 4, 3),
                                (0, 11, 8, 4, 5), (0, 9, 8, 10, None)]),
-                       ("23", [(0, 12, 11, 14, None)])):
+                       ("21", [(1, 11, 10, 12, 6)]),
+                       ("23", [(0, 12, 11, 14, None)]),
+                       ("24", [(1, 12, 11, 13, 2)])):
         env = dict(os.environ, TN_PACK_CAP_LOG2=cap)
         r = subprocess.run([sys.executable, "-c", code.replace("CASES", repr(cases))], capture_output=True,
                            text=True, env=env, cwd=root)
