@@ -1810,6 +1810,13 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     TabPool pool;
     std::vector<void*> ptrs = {const_cast<void*>(l_first ? A : B), const_cast<void*>(l_first ? B : A), C};
     std::vector<void*> allocs;
+    struct FreeOnExit {                 // scratch goes back to the pool on every exit path
+      std::vector<void*>& v;
+      cudaStream_t s;
+      ~FreeOnExit() {
+        for (void* p : v) cudaFreeAsync(p, s);
+      }
+    } free_on_exit{allocs, st};
     auto dalloc = [&](size_t bytes) {
       void* p = nullptr;
       CK(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
@@ -1874,7 +1881,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       else launch_wave<double>(w, ptrs_d, tab_d, st);
       CK(cudaStreamSynchronize(st));
     }
-    for (void* p : allocs) CK(cudaFreeAsync(p, st));
+    // (scratch freed by free_on_exit)
   });
 }
 

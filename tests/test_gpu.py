@@ -667,3 +667,20 @@ def test_degenerate_circuits_on_gpu():
                 assert abs(g - amp(x)) <= tol, (c.name, dtype, x, g, amp(x))
                 assert abs(g - contract_tree(on, osteps, x)) <= tol
                 assert plan.contract(x, 0, 0) == 0
+
+
+def test_pair_misaligned_output_is_an_error_not_a_crash():
+    """tn.h: C must be 16-byte aligned on the tensor-core pair path (TMA stores).  A C
+    view 8 bytes off is refused with an error (TN_ECUDA from the tensor-map encode), the
+    library stays usable, and the next aligned call is correct."""
+    dev = _cuda()
+    nb, m, n, k = 0, 8, 7, 6
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k)
+    A = torch.randn(1 << (m + k), dtype=torch.complex64, device=dev)
+    B = torch.randn(1 << (n + k), dtype=torch.complex64, device=dev)
+    Cbuf = torch.zeros((1 << (m + n)) + 1, dtype=torch.complex64, device=dev)
+    with pytest.raises(tb.TnError):
+        tb.contract_pair(tb.TN_C64, A.data_ptr(), ia, B.data_ptr(), ib, Cbuf[1:].data_ptr(), ic, dims, tb.TN_PATH_TC)
+    torch.cuda.synchronize()
+    got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=3)
+    assert np.all(np.abs(got - ref) <= c64_tol(2 ** k) * bound + 1e-30)
