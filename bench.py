@@ -433,7 +433,10 @@ def run_ours(args):
             roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[2^18][2^12] = A[2^18][2^12] B[2^12][2^12] "
                                                "(one K-slab of the configs[1] (18, 12, 16) steps)",
                                      "dram_bytes": 5.715e10 + 8.663e9, "algorithmic_bytes": 1.731e10,
-                                     "tensor_active": 0.930, "source": "profiles/r01/ncu_full_summary.md"}
+                                     "tensor_active": 0.930, "source": "profiles/r01/ncu_full_summary.md",
+                                     "note": "A panels re-read ~6x from DRAM (L2 hit 79%); the kernel is tensor-bound "
+                                             "(DRAM 11% busy) but power-capped, so raster groups / serpentine order / "
+                                             "K-chunks were tuned to cut these bytes (DESIGN.md)"}
     else:
         roof = {"bound": "hbm", "achieved": small_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
