@@ -5,7 +5,7 @@
 //   C[b][m][n] = sum_k A[b][m][k] * B[b][k][n].
 //
 // Precision scheme: every fp32 component x of A and B
-// is scaled by a power of two per (row, 64-element K chunk) so the chunk maximum lies
+// is scaled by a power of two per (row, 128-element K chunk) so the chunk maximum lies
 // just below 2^14, then split into two fp16 pieces x = x0 + x1 (x0 = fp16(x),
 // x1 = fp16(x - x0)): 22 significand bits, the representation error is
 // <= 2^-24 |x| + 2^-39 max|chunk|.  The three products x0 y0, x0 y1, x1 y0 are
@@ -64,7 +64,7 @@ __device__ __forceinline__ int pack_slot(int q) { return q ^ ((((q >> 4) ^ (q >>
 // exponent with max|x| < 2^e, so the scaled chunk lies in (-2^14, 2^14): the top of the
 // fp16 range, which keeps the second piece of elements far below the chunk maximum out
 // of the fp16 subnormals (absolute floor 2^-25 * 2^-14 of the chunk maximum).
-constexpr int SCALE_LOG2 = 6;   // 64-element K chunks = 2 GEMM stages per TMEM promotion
+constexpr int SCALE_LOG2 = 7;   // 128-element K chunks = 4 GEMM stages per TMEM promotion
 
 // split two scaled floats into two fp16x2 pieces: hi = fp16(x), lo = fp16(x - hi)
 __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_t& p1) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 }
 
 // out planes, layout [b][4][r][k] fp16, plane = 2 * piece + {0: re, 1: im}; scales
-// [b][K / 64][r] fp32 (one per row and 64-element K chunk; one per row if K < 64).
+// [b][K / 128][r] fp32 (one per row and 128-element K chunk; one per row if K < 128).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
 // inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
 __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
@@ -162,7 +162,7 @@ namespace tc {
 
 constexpr int BM = 128;    // rows per tile (TMEM lanes)
 constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
-constexpr int PROMO = 2;   // stages per TMEM accumulation = one 64-element scale chunk
+constexpr int PROMO = 4;   // stages per TMEM accumulation = one 128-element scale chunk
 // CTA rasterization: GROUP_M M-tiles sweep the N tiles together (panels shared in L2).
 // Measured with scripts/raster_sweep.sh (DRAM traffic costs clock under the power cap):
 // pair kernel 4 (DRAM reads 67 -> 55 GB on a (2^18, 2^12, 2^12) step, 1-2% faster);
@@ -522,10 +522,10 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, uint64_t* full, uint64_t
 // Complex GEMM C[b][m][n] (+)= sum_k A[b][m][k] B[b][n][k] on block-scaled fp16x2
 // operands.  Per 32-wide K stage the MMA warp issues
 // 2 (k16) x 3 piece pairs (hi.hi, hi.lo, lo.hi) x 4 real products = 24 MMAs; every
-// 2 stages (one 64-wide scale chunk) go into a fresh TMEM buffer, which the epilogue
+// 4 stages (one 128-wide scale chunk) go into a fresh TMEM buffer, which the epilogue
 // warps promote into fp32 registers, multiplying by the chunk scales sA[row] * sB[col]
 // (round-to-nearest; tcgen05 fp32 accumulation truncates, so no accumulator sees more
-// than 24 updates).  Two TMEM buffers ping-pong.
+// than 48 updates).  Two TMEM buffers ping-pong.
 template <int BN>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     cgemm_f16x2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,

@@ -641,8 +641,8 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   };
   std::vector<char> inT(D, 0);
   int t = 0;
-  for (int j = 0; j < std::min(6, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
-  for (int j = 0; j < D; ++j) if (pi[j] < 5 && !inT[j]) { inT[j] = 1; ++t; }
+  for (int j = 0; j < std::min(tnd::SCALE_LOG2, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
+  for (int j = 0; j < D; ++j) if (pi[j] < 4 && !inT[j]) { inT[j] = 1; ++t; }
   for (int j = 0; j < D && t < std::min(tnd::PACK_MAX_T, D); ++j) if (!inT[j]) { inT[j] = 1; ++t; }
   if (t < 3 || (planes == 4 && (t < 8 || k_lo < 4)))
     throw Err(TN_EUNSUPPORTED, "tensor-core pack needs >= 256 elements and K >= 16 per operand");
@@ -746,7 +746,7 @@ int64_t pack_bytes(const TcStep& t, int rows_bits) {
   // 4 fp16 planes + one fp32 scale per row and 64-wide K chunk (+ slack: the GEMM's
   // scale copies read whole 128-row / BN-column tiles)
   return (int64_t(8) << (t.nb_bits + rows_bits + t.k_lo)) +
-         (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - 6, 0))) + 1024;
+         (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - tnd::SCALE_LOG2, 0))) + 1024;
 }
 
 // first-fit offsets for (size, [lo, hi]) items

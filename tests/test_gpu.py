@@ -138,7 +138,7 @@ def _wide_range(shape, seed, dtype):
     """complex Gaussian entries times 2^u, u uniform in [-12, 12] per entry, with some
     exact zeros and a few entries scaled by 1e-25: the block-scaled fp16x2 split
     must stay at fp32 level relative to sum_k |A||B| (the
-    representation floor is 2^-39 of the 64-element chunk maximum, so the guarantee needs
+    representation floor is 2^-39 of the 128-element chunk maximum, so the guarantee needs
     the dynamic range inside a chunk to stay well below 2^39; 2^24 here)."""
     g = np.random.default_rng(seed)
     x = _rand(shape, seed, dtype).astype(np.complex128)
@@ -153,10 +153,10 @@ def _wide_range(shape, seed, dtype):
 @pytest.mark.parametrize("case", [(0, 7, 8, 9), (1, 6, 7, 12), (0, 7, 7, 4)])
 def test_pair_tensor_core_wide_dynamic_range(case):
     """Block-scaled fp16x2 error model: each element x of a
-    64-wide K chunk with maximum mx (over re and im) is represented to
+    128-wide K chunk with maximum mx (over re and im) is represented to
     <= 2^-24 |x| + 2^-38 mx, the dropped x1 y1 is <= 2^-24 |x y|, so
     |C - C_ref| <= tol(K) sum_k |A||B| + 2^-37 sum_k (mA |B| + |A| mB).
-    Unpermuted layouts, so the chunks are consecutive runs of 64 along K."""
+    Unpermuted layouts, so the chunks are consecutive runs of 128 along K."""
     nb, m, n, k = case
     ia, ib, ic, dims = _gemm_case(nb, m, n, k)
     got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_TC, seed=40, gen=_wide_range)
@@ -164,7 +164,7 @@ def test_pair_tensor_core_wide_dynamic_range(case):
     B_, M_, N_, K_ = 1 << nb, 1 << m, 1 << n, 1 << k
     A = _wide_range([2] * len(ia), 40, tb.TN_C64).reshape(B_, M_, K_).astype(np.complex128)
     Bm = _wide_range([2] * len(ib), 41, tb.TN_C64).reshape(B_, K_, N_).astype(np.complex128)
-    ch = min(64, K_)
+    ch = min(128, K_)               # the scale chunk (SCALE_LOG2 = 7)
     cm = lambda X: np.maximum(np.abs(X.real), np.abs(X.imag))
     mA = np.repeat(cm(A).reshape(B_, M_, K_ // ch, ch).max(axis=3), ch, axis=2)           # [b][m][k]
     mB = np.repeat(cm(Bm).reshape(B_, K_ // ch, ch, N_).max(axis=2), ch, axis=1)          # [b][k][n]
@@ -175,10 +175,11 @@ def test_pair_tensor_core_wide_dynamic_range(case):
 
 
 def _zero_chunks(shape, seed, dtype):
-    """Gaussian entries with every other run of 64 consecutive elements set to zero."""
+    """Gaussian entries with every other run of 128 consecutive elements (one scale
+    chunk) set to zero."""
     x = _rand(shape, seed, dtype).reshape(-1).copy()
-    for j in range(0, x.size, 128):
-        x[j:j + 64] = 0
+    for j in range(0, x.size, 256):
+        x[j:j + 128] = 0
     return x.reshape(shape)
 
 
