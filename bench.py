@@ -427,14 +427,14 @@ def run_ours(args):
         if dtype == tb.TN_C64:
             # DRAM traffic (bytes) of one launch of the bench's dominant GEMM shape from the
             # committed ncu --set full capture: a K-slab of the (18, 12, 16) steps (64% of a
-            # configs[1] step).  A is re-read ~6x from DRAM (L2 hit 79%), harmless for a
+            # configs[1] step).  A is re-read ~5x from DRAM (L2 hit 78%), harmless for a
             # tensor-bound kernel (DRAM at 13%)
-            roof["traffic"] = 5.715e10 + 8.663e9
+            roof["traffic"] = 5.025e10 + 8.661e9
             roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[2^18][2^12] = A[2^18][2^12] B[2^12][2^12] "
                                                "(one K-slab of the configs[1] (18, 12, 16) steps)",
-                                     "dram_bytes": 5.715e10 + 8.663e9, "algorithmic_bytes": 1.731e10,
+                                     "dram_bytes": 5.025e10 + 8.661e9, "algorithmic_bytes": 1.731e10,
                                      "tensor_active": 0.930, "source": "profiles/r01/ncu_full_summary.md",
-                                     "note": "A panels re-read ~6x from DRAM (L2 hit 79%); the kernel is tensor-bound "
+                                     "note": "A panels re-read ~5x from DRAM (L2 hit 78%); the kernel is tensor-bound "
                                              "(DRAM 11% busy) but power-capped, so raster groups / serpentine order / "
                                              "K-chunks were tuned to cut these bytes (DESIGN.md)"}
     else:
