@@ -336,7 +336,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "r"(taddr));
 }
 
-// Epilogue warps of both GEMM kernels: promote every TMEM accumulation (one 64-wide
+// Epilogue warps of both GEMM kernels: promote every TMEM accumulation (one 128-wide
 // scale chunk) into fp32 registers, scaled by sA[row] * sB[col], then write C rows
 // [row0, row0 + 128) x columns [col0, col0 + BN) (C += when `acc_c`); C is addressed as
 // [b][c_rows][N] with this launch's rows at c_row_off (row slabs of a larger C).  kPair: the

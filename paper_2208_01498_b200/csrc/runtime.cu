@@ -743,7 +743,7 @@ void finish_cuda_core(TcStep& t, int dtype, int kind) {
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
   if (t.kind != K_TC) return int64_t(t.esz) << (t.nb_bits + rows_bits + t.k_lo);
-  // 4 fp16 planes + one fp32 scale per row and 64-wide K chunk (+ slack: the GEMM's
+  // 4 fp16 planes + one fp32 scale per row and 128-wide K chunk (+ slack: the GEMM's
   // scale copies read whole 128-row / BN-column tiles)
   return (int64_t(8) << (t.nb_bits + rows_bits + t.k_lo)) +
          (int64_t(4) << (t.nb_bits + rows_bits + std::max(t.k_lo - tnd::SCALE_LOG2, 0))) + 1024;
