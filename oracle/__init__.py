@@ -19,6 +19,7 @@ Modules
   statevector brute-force state-vector simulation (independent check).
   bounds      Theorem 1 / 2 closed forms and constants (l.57, l.94, l.109, l.118).
 
-Parity status: every function is pinned by tests in tests/test_oracle_*.py against
+Parity status: every function is pinned by tests in tests/test_oracle.py and
+tests/test_oracle_ssa_pins.py (mutation check: scripts/oracle_mutations.sh) against
 brute force, closed forms and invariants.
 """

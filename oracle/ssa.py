@@ -274,6 +274,8 @@ class _Ctx:
         self.steps = []
         self.n_leaves = len(net.tensors)
         self.log = []
+        self.seps = []        # (ids, separator, E, I) of every SSA split, for the pins
+        self.leaves = []      # ids of every greedy leaf, for the pins
 
 
 def assign_boundary(ctx, ids, lab):
@@ -326,7 +328,8 @@ def assign_boundary(ctx, ids, lab):
 
 
 def find_separator(ctx, ids, rng):
-    """Algorithm 1 steps 1-7 on the tensors `ids`; returns (E, I, info) or None."""
+    """Algorithm 1 steps 1-7 on the tensors `ids`; returns None or
+    (E, I, (max open bits, cut), tries, (|O|, |E|, |I|), separator)."""
     s = len(ids)
     PX = ctx.PX[ids]
     PY = ctx.PY[ids]
@@ -361,7 +364,7 @@ def find_separator(ctx, ids, rng):
                 continue
             n_ok += 1
             if best is None or cut < best[2]:
-                best = (E, I, cut, tries, (nO, nE, nI))
+                best = (E, I, cut, tries, (nO, nE, nI), sep)
             if n_ok >= ctx.n_valid:
                 break
         if best is not None:
@@ -437,6 +440,7 @@ def greedy_leaf(ctx, ids):
 
 def _build(ctx, ids, sid, depth):
     if len(ids) <= ctx.leaf_size:
+        ctx.leaves.append(list(ids))
         return greedy_leaf(ctx, ids)
     rng = Stream(ctx.seed, sid)
     res = find_separator(ctx, ids, rng)
@@ -444,8 +448,9 @@ def _build(ctx, ids, sid, depth):
         E, I = median_split(ctx, ids)
         ctx.log.append((depth, len(ids), "median"))
     else:
-        E, I, cut, tries, _cnt = res
+        E, I, cut, tries, _cnt, sep = res
         ctx.log.append((depth, len(ids), cut, tries))
+        ctx.seps.append((list(ids), sep, E, I))
     nE = _build(ctx, E, child_stream(sid, 0), depth + 1)
     nI = _build(ctx, I, child_stream(sid, 1), depth + 1)
     return _merge(ctx, nE, nI)

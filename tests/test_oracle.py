@@ -326,25 +326,6 @@ def test_centerpoint_brute_force_depth():
         assert worst * 4 >= 14 - 4, worst       # (d+1+delta):1 depth with the 2-point slack
 
 
-def test_separator_satisfies_eqs_1_2_on_grid():
-    """20x20 grid network: every SSA separator meets Eq. (1) and Eq. (2)."""
-    c = lattice_cz(10, 10, 4, 71)
-    net = build_network(c)
-    ctx = ssa._Ctx(net, 0, 8, 32, 8, 64)
-    ids = list(range(len(net.tensors)))
-    res = ssa.find_separator(ctx, ids, Stream(0, 1))
-    assert res is not None
-    E, I, key, tries, (nO, nE, nI) = res
-    assert sorted(E + I) == ids and not set(E) & set(I) and E and I
-    s = len(ids)
-    assert nO + nE + nI == s
-    assert nO <= 2.0 * math.sqrt(net.k_bound) * math.sqrt(s)        # Eq. (1), c_2 = 2
-    assert 4 * nE <= 3 * s and 4 * nI <= 3 * s                     # Eq. (2), (d+1)/(d+2) = 3/4
-    # Gamma_E and Gamma_I spheres do not intersect (SST)
-    PX, PY, r = ctx.PX, ctx.PY, net.radius
-    lab = {t: 0 for t in ids}
-
-
 def test_order_is_a_binary_tree_and_deterministic():
     c = lattice_cz(4, 4, 8, 0)
     net = build_network(c)
