@@ -4,17 +4,27 @@ amplitudes/s on B200, % of tensor-pipe peak).
 
 Default workload (N=1): configs[1] -- 8x8 qubit lattice, depth 16, Haar U(2) + CZ
 brickwork, complex64 on block-scaled fp16x2 split-precision tensor cores, separator
-order (SM Algorithm 1) sliced so every tensor fits HBM.  Its amplitudes are partitioned
-by bitstring across ranks (weak scaling): rank r contracts bitstrings r, r+N, ... of the
-seeded batch of 1024.  One STEP = one slice of one amplitude (the whole separator tree
-over one sliced sub-network); an amplitude is n_slices steps.  Intermediates are GBs,
-far larger than the 126 MB L2, so no L2 flush is needed between steps.
+order (SM Algorithm 1, best of 256 randomized hierarchies) sliced to 2^34-entry tensors.
+Its batch of 1024 seeded bitstrings is split into contiguous blocks per rank (weak
+scaling, no data-path collective; paper_2208_01498_b200/dist.py).  One STEP = one
+contributing slice of one amplitude (the whole separator tree over one sliced
+sub-network); a rank walks its bitstrings, each through its contributing slices.
+Intermediates are GBs, far larger than the 126 MB L2, so no L2 flush is needed.
 
 --config 2 / 4 (Sycamore-53 m=14, (2+1)D 12x12 depth 20; complex64): one amplitude,
-its slices partitioned across ranks (rank r takes slices [r K, (r+1) K) of the K timed
-steps), the per-rank partial amplitudes summed by ONE NCCL all-reduce inside the timed
-region.  --config 3 (IQP 10x10, complex128 on the FP64 tensor pipe): one STEP = one
-full amplitude (unsliced), bitstrings r::N of 256 per rank.
+its contributing slices split into disjoint contiguous blocks per rank, the per-step
+partial amplitudes summed over ranks by ONE all-reduce (NCCL) inside the timed region.
+--config 3 (IQP 10x10, complex128 on the FP64 tensor pipe): one STEP = one full
+amplitude (unsliced), contiguous blocks of the 256 bitstrings per rank.
+
+The timed steps go through tn_contract_profiled (eager launches, CUDA events per kernel
+class); their per-step amplitudes are checked against the CUDA-graph path
+(tn_contract_device) for the same (bitstring, slice) after the timed region.
+
+--impl reference: the oracle (numpy complex128, oracle/) on the host cores, along the
+oracle's own order for the workload (oracle/orders/config<C>.json, written by
+scripts/write_oracle_orders.py with oracle.ssa.find_order only); it does not load the
+product library.
 
   python bench.py [--gpus N --steps K --warmup W] [--config C] [--impl reference]
 Prints ONE JSON line (rank 0).
@@ -37,18 +47,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "contraction FLOP/s"
 ORDER_SEED = 0
-# per config: arithmetic type, how the units shard across ranks, slicing targets tried in
-# order (largest tensor of a slice 2^t entries; the first plan that fits HBM is used)
-# n_seeds: randomized separator hierarchies built, the one with the least Eq. (3) work of
-# all slices kept (R10) -- for sliced configs the slicing overhead varies by
-# orders of magnitude between hierarchies (configs[1]: 2^59.2 with 4, 2^56.7 with 64,
-# 2^54.6 with 256; built on host threads, ~10 s)
+# per config: arithmetic type, how the units shard across ranks, slicing target (largest
+# tensor of a slice 2^t entries, chosen so the plan's arena fits 180 GB), randomized
+# separator hierarchies built (the one with the least Eq. (3) work of all slices kept,
+# DESIGN.md R10: the slicing overhead differs by orders of magnitude between
+# hierarchies), the IQP hyperedge reading R3.  Must equal scripts/write_oracle_orders.py.
 SPEC = {
-    1: dict(dtype="c64", shard="bits", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
-    2: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=256),
-    3: dict(dtype="c128", shard="bits", slice_logs=(0,), hyper=True, n_seeds=4),
-    4: dict(dtype="c64", shard="slices", slice_logs=(34, 33, 32, 31), hyper=False, n_seeds=1024),
+    1: dict(dtype="c64", shard="bits", slice_log=34, hyper=False, n_seeds=256),
+    2: dict(dtype="c64", shard="slices", slice_log=33, hyper=False, n_seeds=256),
+    3: dict(dtype="c128", shard="bits", slice_log=0, hyper=True, n_seeds=4),
+    4: dict(dtype="c64", shard="slices", slice_log=32, hyper=False, n_seeds=1024),
 }
+ORDERS = os.path.join(ROOT, "oracle", "orders")
+TRAFFIC = os.path.join(ROOT, "profiles", "r02", "traffic.json")
 # complex128 GEMM on DMMA: MEASURED_PEAKS.json has no fp64 figure; our own probe
 # (scripts/probes/dmma_peak.cu, profiles/r01/fp64_tensor_peak.md) measured 37.0 TF/s of
 # back-to-back register-only mma.sync f64 on this pool's B200 (burst clock)
@@ -179,13 +190,54 @@ def workload(ci):
     return c, bits
 
 
-def cpu_baseline_sample(c, bits, steps, sl, budget_s=15.0, hyper=False):
-    """The oracle as it stands on the host cores: slice 0 of bitstring 0 of the same
-    network and the same order (the step list and sliced indices of the plan, from
-    tn_find_order -- the oracle's own find_order builds the identical order, bit for
-    bit, but takes minutes in Python for 64 hierarchies), contracting the steps of the
-    separator tree in order with oracle.contract.contract_pair until `budget_s` of CPU
-    time; FLOP/s = sum 8 M / elapsed."""
+def oracle_order(ci):
+    """The workload's separator order as the ORACLE found it (oracle/orders/, written by
+    scripts/write_oracle_orders.py; tn_find_order reproduces it bit for bit,
+    tests/test_library_host.py)."""
+    path = os.path.join(ORDERS, f"config{ci}.json")
+    with open(path) as f:
+        o = json.load(f)
+    spec = SPEC[ci]
+    assert (o["seed"], o["n_seeds"], o["max_log2_size"], o["diag_hyper"]) == \
+        (ORDER_SEED, spec["n_seeds"], spec["slice_log"], spec["hyper"]), f"{path} does not match SPEC[{ci}]"
+    return o
+
+
+def workload_name(ci, c):
+    spec = SPEC[ci]
+    return (f"configs[{ci}]: {c.name}; separator order seed {ORDER_SEED}, best of {spec['n_seeds']} randomized "
+            f"hierarchies" + (f"; slicing to 2^{spec['slice_log']}-entry tensors" if spec["slice_log"] else ""))
+
+
+def shared_config(ci, c, n_bits, slice_bits, flops_slice):
+    """`config` of the JSON line, identical for both arms: the workload, what one step
+    is, and its Eq. (3) flops (8 M per pairwise step, R13) -- all fixed by the circuit and
+    the order, none by the implementation."""
+    spec = SPEC[ci]
+    if spec["shard"] == "slices":
+        step = (f"one contributing slice (of 2^{slice_bits}) of one amplitude; ranks take disjoint contiguous blocks "
+                f"of its slices, per-step partial amplitudes summed by one all-reduce in the timed region")
+    elif slice_bits:
+        step = (f"one contributing slice (of 2^{slice_bits}) of one amplitude; the batch of {n_bits} bitstrings in "
+                f"contiguous blocks per rank, each bitstring through its contributing slices")
+    else:
+        step = f"one full amplitude (unsliced); the batch of {n_bits} bitstrings in contiguous blocks per rank"
+    return {"workload": workload_name(ci, c), "step": step, "flops_per_step": flops_slice, "slice_bits": slice_bits,
+            "l2": "working set (intermediates of GBs) >> 126 MB L2, no flush between steps"}
+
+
+def oracle_flops_per_slice(net, o):
+    """8 x (Eq. (3) multiplications of one slice) from the oracle's own order."""
+    from oracle.ssa import sliced_work
+    return 8.0 * sliced_work(net, [tuple(p) for p in o["steps"]], o["slices"]) / 2.0 ** o["slice_bits"]
+
+
+def cpu_baseline_sample(c, bits, o, budget_s=15.0, hyper=False):
+    """The oracle as it stands on the host cores: slice 0 of bitstring 0 along the
+    oracle's own order (oracle/orders/), contracting the steps of the separator tree in
+    order with oracle.contract.contract_pair (numpy complex128) until `budget_s` of
+    wall time; FLOP/s = sum 8 M / elapsed.  Steps too large for the budget (M > 2^33)
+    and the steps depending on them are skipped."""
     from oracle.network import build_network
     from oracle.contract import kept_per_step, leaf_tensors, contract_pair
     try:
@@ -194,6 +246,8 @@ def cpu_baseline_sample(c, bits, steps, sl, budget_s=15.0, hyper=False):
     except Exception:
         cores = os.cpu_count()
     net = build_network(c, diag_hyper=hyper)
+    steps = [tuple(p) for p in o["steps"]]
+    sl = o["slices"]
     kept = kept_per_step(net, steps)
     fixed = {i: 0 for i in sl}
     n = len(net.tensors)
@@ -222,17 +276,9 @@ def cpu_baseline_sample(c, bits, steps, sl, budget_s=15.0, hyper=False):
             break
     el = time.perf_counter() - t0
     return {"value": flops / el, "unit": "FLOP/s", "cores": int(cores), "kind": "oracle", "elapsed_s": el,
-            "sample": f"oracle (numpy complex128) on slice 0 of bitstring 0: {done} of the {len(steps)} pairwise "
-                      f"steps of the separator tree in order, skipping {skipped} steps with M > 2^33 or depending on "
-                      f"one ({flops:.3g} flops, {el:.1f} s)"}
-
-
-def workload_name(ci, c, slice_log2):
-    spec = SPEC[ci]
-    prec = "block-scaled fp16x2 split on tcgen05" if spec["dtype"] == "c64" else "FP64 tensor pipe (DMMA)"
-    return (f"configs[{ci}]: {c.name}; {spec['dtype']} ({prec}); separator order seed {ORDER_SEED}, "
-            f"best of {spec['n_seeds']} randomized hierarchies"
-            + (f"; slicing to 2^{slice_log2}-entry tensors" if slice_log2 else ""))
+            "sample": f"oracle (numpy complex128, plain einsum pairs) on slice 0 of bitstring 0 along the oracle's "
+                      f"own order: {done} of the {len(steps)} pairwise steps in order, skipping {skipped} with "
+                      f"M > 2^33 or depending on one ({flops:.3g} flops, {el:.1f} s)"}
 
 
 def run_reference(args):
@@ -241,26 +287,36 @@ def run_reference(args):
         return 0
     spec = SPEC[args.config]
     c, bits = workload(args.config)
-    import paper_2208_01498_b200 as tb       # host-only calls: network + order (no device)
-    net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
-    order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=spec["slice_logs"][0])
+    from oracle.network import build_network
+    o = oracle_order(args.config)
+    net = build_network(c, diag_hyper=spec["hyper"])
+    cfg = shared_config(args.config, c, len(bits), o["slice_bits"], oracle_flops_per_slice(net, o))
     vals = []
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline_sample(c, bits, order.steps(), order.slices(),
-                                        budget_s=max(2.0, 60.0 / (args.warmup + args.steps)), hyper=spec["hyper"]))
+        vals.append(cpu_baseline_sample(c, bits, o, budget_s=max(2.0, 60.0 / (args.warmup + args.steps)),
+                                        hyper=spec["hyper"]))
     timed = vals[args.warmup:]
     v = float(np.mean([t["value"] for t in timed]))
-    cfg = {"workload": workload_name(args.config, c, spec["slice_logs"][0]),
-           "step": "a bounded sample of one slice's pairwise steps (see cpu_baseline.sample)"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "FLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.mean([t["elapsed_s"] for t in timed])), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": cfg,
+            "arithmetic": "numpy complex128 on the host (the oracle); each step a bounded sample of the workload's "
+                          "step (cpu_baseline.sample)",
             "cpu_baseline": {"value": v, "unit": "FLOP/s", "cores": timed[0]["cores"], "kind": "oracle",
                              "sample": timed[0]["sample"]},
             "e2e": {"value": v, "unit": "FLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+def load_traffic(ci):
+    """DRAM traffic of the dominant kernel per launch from a committed ncu --set full
+    capture (profiles/r02/traffic.json, written by scripts/traffic_from_ncu.py)."""
+    try:
+        return json.load(open(TRAFFIC)).get(f"config{ci}")
+    except Exception:
+        return None
 
 
 def run_ours(args):
@@ -272,62 +328,59 @@ def run_ours(args):
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
         os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (no version banner)
     if distributed:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2208_01498_b200 as tb
+    from paper_2208_01498_b200 import dist as pdist
 
     ci = args.config
     spec = SPEC[ci]
     c, bits = workload(ci)
     dtype = tb.TN_C64 if spec["dtype"] == "c64" else tb.TN_C128
     net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
-    plan = None
-    for slice_log2 in spec["slice_logs"]:
-        order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=slice_log2)
-        try:
-            plan = tb.Plan(net, order, dtype=dtype, device=local)
-            break
-        except tb.TnError as e:       # arena does not fit this GPU: slice further
-            print(f"slicing target 2^{slice_log2}: {e}", file=sys.stderr)
-    if plan is None:
-        raise RuntimeError("no slicing target fits device memory")
+    order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=spec["slice_log"])
+    oinfo = order.info()
+    plan = tb.Plan(net, order, dtype=dtype, device=local)      # raises if the arena does not fit
     pinfo = plan.info()
     n_slices = int(pinfo["n_slices"])
     slice_bits = int(pinfo["slice_bits"])
     flops_slice = float(pinfo["flops_per_slice"])
     by_slices = spec["shard"] == "slices"
-    # one step: one slice (sliced configs) or one whole amplitude (unsliced)
-    step_slices = 1 if n_slices > 1 else n_slices
-    my_bits = bits[0:1] if by_slices else bits[rank::ws]
-    bits_dev = torch.from_numpy(np.ascontiguousarray(my_bits)).to(dev)
-    nq = c.n
-    amp = torch.zeros(1, dtype=torch.complex128, device=dev)
+    K, W = args.steps, args.warmup
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
-    # steps run contributing slices only (provably zero ones are skipped by tn_contract /
-    # tn_amplitudes, so they are not work an amplitude needs)
-    total_steps = args.steps + args.warmup
-    if by_slices:       # rank r: contributing slices [r K, (r + 1) K) of one amplitude, then warm-ups
-        live = plan.contributing_slice_ids(my_bits[0], 0, (ws + 1) * total_steps)
-        mine = live[rank * args.steps:(rank + 1) * args.steps] + live[ws * args.steps:ws * args.steps + args.warmup]
-    elif n_slices > 1:  # config 1: contributing slices of this rank's first bitstring
-        mine = plan.contributing_slice_ids(my_bits[0], 0, total_steps)
+    # ---- work items (row of the batch, slice id): one per step, from dist.py ----
+    if by_slices:
+        live = plan.contributing_slice_ids(bits[0], 0, ws * K)
+        mine = pdist.slice_block(live, ws, rank)
+        if not mine:
+            raise RuntimeError(f"rank {rank}: no slice to contract ({len(live)} contributing slices for {ws} ranks)")
+        items = [(0, s) for s in mine]
+        warm = [items[j % len(items)] for j in range(W)]
+        n_units_all = len(live)
     else:
-        mine = [0]
-    mine = (mine * (total_steps // max(len(mine), 1) + 1))[:total_steps]
-
-    def step_args(j):
-        """(bitstring row, first slice) of this rank's j-th step (j >= steps: warm-ups)"""
+        lo, hi = pdist.block_range(len(bits), ws, rank)
+        rows = list(range(lo, hi))
         if n_slices > 1:
-            return 0, mine[j]
-        return j % len(my_bits), 0
+            items = pdist.bitstring_steps(lambda r, n: plan.contributing_slice_ids(bits[r], 0, n), rows, K + W)
+        else:
+            items = [(r, 0) for r in rows[:K + W]]
+        if len(items) < K + W:
+            raise RuntimeError(f"rank {rank}: {len(items)} work items for {K + W} steps")
+        warm, items = items[K:], items[:K]
+        n_units_all = K * ws
+    steps_mine = len(items)
+    bits_dev = torch.from_numpy(np.ascontiguousarray(bits)).to(dev)
+    # one complex128 accumulator per step (the same length K on every rank: the all-reduce of
+    # the sliced configs sums them elementwise over ranks)
+    amp = torch.zeros(max(K, 1), dtype=torch.complex128, device=dev)
+    scratch = torch.zeros(1, dtype=torch.complex128, device=dev)
 
-    for w in range(args.warmup):
-        row, sl = step_args(args.steps + w)
-        plan.contract_device(bits_dev[row].data_ptr(), sl, sl + step_slices, amp.data_ptr(), sptr)
+    for row, s in warm:
+        plan.contract_device(bits_dev[row].data_ptr(), s, s + 1, scratch.data_ptr(), sptr)
     torch.cuda.synchronize()
 
     def barrier():
@@ -335,69 +388,81 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- timed region: K steps through the profiled launcher (+ the slice all-reduce) ----
-    amp.zero_()
+    # ---- timed region: the steps through the profiled launcher (+ the slice all-reduce) ----
     launches0 = tb.kernel_launches()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record(stream)
-        prof = {}
-        for j in range(args.steps):
-            row, sl = step_args(j)
-            p = plan.contract_profiled(bits_dev[row].data_ptr(), sl, sl + step_slices, amp.data_ptr(), sptr)
-            for k, v in p.items():
-                prof[k] = prof.get(k, 0) + v
-        if by_slices and distributed:
-            torch.distributed.all_reduce(amp)        # partial amplitudes of all ranks' slices
+        prof = None
+        for j, (row, s) in enumerate(items):
+            p = plan.contract_profiled(bits_dev[row].data_ptr(), s, s + 1, amp[j:j + 1].data_ptr(), sptr)
+            if prof is None:
+                prof = p
+            else:
+                for k, v in p.items():
+                    if k == "kernels":
+                        for name, d in v.items():
+                            for f, x in d.items():
+                                prof["kernels"][name][f] += x
+                    else:
+                        prof[k] += v
+        if by_slices:
+            amp_mine = amp.clone()                  # (this rank's values, for the check below)
+            pdist.allreduce_sum_(amp)               # partial amplitudes of all ranks' slices
         e1.record(stream)
         barrier()
     launches = tb.kernel_launches() - launches0
-    ms = e0.elapsed_time(e1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if distributed:
-        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t_max.item())
-    flops_step = flops_slice * step_slices
-    total_flops = flops_step * args.steps * ws
+    ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    total_flops = flops_slice * n_units_all
     value = total_flops / (ms / 1e3)
-    # an amplitude = its contributing slices (provably zero ones are skipped by
-    # tn_contract / tn_amplitudes); this rank's first bitstring
-    contrib = plan.contributing_slices(my_bits[0]) if n_slices > 1 else 1
-    amps_per_s = value / (flops_slice * contrib)
+
+    # ---- the timed amplitudes against the CUDA-graph path (same bitstring and slice) ----
+    n_chk = min(steps_mine, 2)
+    chk = torch.zeros(max(n_chk, 1), dtype=torch.complex128, device=dev)
+    for j in range(n_chk):
+        row, s = items[j]
+        plan.contract_device(bits_dev[row].data_ptr(), s, s + 1, chk[j:j + 1].data_ptr(), sptr)
+    torch.cuda.synchronize()
+    a_t, a_g = (amp_mine if by_slices else amp)[:n_chk].cpu().numpy(), chk[:n_chk].cpu().numpy()
+    rel = float(np.max(np.abs(a_t - a_g) / np.maximum(np.abs(a_g), 1e-300))) if n_chk else 0.0
+    if not rel <= 1e-9:
+        raise RuntimeError(f"timed (profiled) amplitudes differ from the graph path: {a_t} vs {a_g}")
+
+    # amplitudes/s: an amplitude needs its contributing slices (provably zero ones are
+    # skipped by tn_contract / tn_amplitudes); mean over the whole batch
+    if n_slices > 1:
+        contrib_mean = float(np.mean([plan.contributing_slices(b) for b in bits]))
+    else:
+        contrib_mean = 1.0
+    amps_per_s = value / (flops_slice * contrib_mean)
 
     # ---- e2e: the public host-buffer call, H2D bits (pinned host memory) + D2H amplitude
     # inside the region ----
-    e2e_steps = max(1, min(args.steps, 3))
-    pinned = torch.from_numpy(np.ascontiguousarray(my_bits)).pin_memory().numpy()
+    e2e_items = items[:max(1, min(K, 3))]
+    pinned = torch.from_numpy(np.ascontiguousarray(bits)).pin_memory().numpy()
     barrier()
     t0 = time.perf_counter()
-    for j in range(e2e_steps):
-        row, sl = step_args(j)
-        plan.contract(pinned[row], sl, sl + step_slices)
+    for row, s in e2e_items:
+        plan.contract(pinned[row], s, s + 1)
     barrier()
-    e2e_s = time.perf_counter() - t0
-    t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if distributed:
-        torch.distributed.all_reduce(t_e, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = flops_step * e2e_steps * ws / float(t_e.item())
+    e2e_s = pdist.max_over_ranks(time.perf_counter() - t0, dev)
+    e2e_value = flops_slice * len(e2e_items) * ws / e2e_s
 
     # ---- unsliced bitstring configs: throughput of tn_amplitudes with concurrent lanes ----
     lanes_line = None
     if not by_slices and n_slices == 1:
         try:
             plan.set_lanes(4)
-            batch = np.ascontiguousarray(my_bits[:64])
+            lo, hi = pdist.block_range(len(bits), ws, rank)
+            batch = np.ascontiguousarray(bits[lo:hi][:64])
             plan.amplitudes(batch[:8])
             barrier()
             t0 = time.perf_counter()
             plan.amplitudes(batch)
             barrier()
-            dt_l = time.perf_counter() - t0
-            t_l = torch.tensor([dt_l], dtype=torch.float64, device=dev)
-            if distributed:
-                torch.distributed.all_reduce(t_l, op=torch.distributed.ReduceOp.MAX)
-            lanes_line = {"lanes": 4, "amplitudes": int(len(batch)) * ws, "value": len(batch) * ws / float(t_l.item()),
+            dt_l = pdist.max_over_ranks(time.perf_counter() - t0, dev)
+            lanes_line = {"lanes": 4, "amplitudes": int(len(batch)) * ws, "value": len(batch) * ws / dt_l,
                           "unit": "amplitudes/s", "call": "tn_amplitudes (host bitstrings in, host amplitudes out)"}
         except tb.TnError as e:
             print(f"lanes: {e}", file=sys.stderr)
@@ -408,79 +473,76 @@ def run_ours(args):
         return 0
     peaks, peak_src = load_peaks()
     sustained = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    hbm = peaks["hbm_gbs"]
     if dtype == tb.TN_C64:
         peak_tc = sustained / F16_FLOPS_PER_USEFUL
-        kname, pnote = "cgemm_f16x2s_kernel (tcgen05)", (
-            f"{peak_src} bf16 sustained {sustained} TF/s (= fp16 dense rate) x 8/24 (useful complex flops per "
-            "fp16 tensor flop of the fp16x2 scheme)")
+        tc_note = (f"{peak_src} bf16 sustained {sustained} TF/s (= fp16 dense rate) x 8/24 (useful complex flops per "
+                   "fp16 tensor flop of the fp16x2 scheme)")
     else:
         peak_tc = FP64_TC_TFLOPS
-        kname, pnote = "zgemm_dmma_kernel (FP64 tensor pipe, complex128)", (
-            "fp64 tensor peak 37.0 TF/s measured by scripts/probes/dmma_peak.cu (register-only mma.sync f64, "
-            "burst clock; profiles/r01/fp64_tensor_peak.md); complex128 flops are executed flops")
-    gemm_tfs = prof["flops_gemm"] / (prof["ms_gemm"] / 1e3) / 1e12 if prof.get("ms_gemm") else 0.0
-    small_gbs = prof["bytes_small"] / (prof["ms_small"] / 1e3) / 1e9 if prof.get("ms_small") else 0.0
-    if prof.get("ms_gemm", 0) >= prof.get("ms_small", 0):
-        roof = {"bound": "tensor", "achieved": gemm_tfs, "peak": peak_tc, "unit": "TFLOP/s",
-                "frac": gemm_tfs / peak_tc if peak_tc else None, "traffic": None, "kernel": kname,
-                "peak_note": pnote, "share_of_step": prof["ms_gemm"] / ms if ms else None}
-        if dtype == tb.TN_C64:
-            # DRAM traffic (bytes) of one launch of the bench's dominant GEMM shape from the
-            # committed ncu --set full capture: a K-slab of the (18, 12, 16) steps (64% of a
-            # configs[1] step).  A is re-read ~5x from DRAM (L2 hit 78%), harmless for a
-            # tensor-bound kernel (DRAM at 13%)
-            roof["traffic"] = 5.025e10 + 8.661e9
-            roof["traffic_probe"] = {"launch": "cgemm2_f16x2s_kernel, C[2^18][2^12] = A[2^18][2^12] B[2^12][2^12] "
-                                               "(one K-slab of the configs[1] (18, 12, 16) steps)",
-                                     "dram_bytes": 5.025e10 + 8.661e9, "algorithmic_bytes": 1.731e10,
-                                     "tensor_active": 0.930, "source": "profiles/r01/ncu_full_summary.md",
-                                     "note": "A panels re-read ~5x from DRAM (L2 hit 78%); the kernel is tensor-bound "
-                                             "(DRAM 11% busy) but power-capped, so raster groups / serpentine order / "
-                                             "K-chunks were tuned to cut these bytes (DESIGN.md)"}
-    else:
-        roof = {"bound": "hbm", "achieved": small_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": small_gbs / peaks["hbm_gbs"], "traffic": None, "kernel": "small_contract_kernel",
-                "peak_note": f"{peak_src} HBM copy bandwidth; algorithmic bytes = operands + results of each wave",
-                "share_of_step": prof["ms_small"] / ms if ms else None}
+        tc_note = ("fp64 tensor peak 37.0 TF/s measured by scripts/probes/dmma_peak.cu (register-only mma.sync f64, "
+                   "burst clock; profiles/r01/fp64_tensor_peak.md); complex128 flops are executed flops")
+    tensor_classes = {"cgemm_f16x2s_kernel", "cgemm2_f16x2s_kernel", "cgemm2p_f16x2s_kernel", "zgemm_dmma_kernel"}
+    hbm_classes = {"small_contract_kernel", "pack_f16x2s_kernel", "pack_planar_kernel", "skinny_kernel", "wide_kernel"}
+    kern = {}
+    for name, d in prof["kernels"].items():
+        if d["ms"] <= 0:
+            continue
+        r = {"ms": d["ms"], "share_of_step": d["ms"] / ms}
+        if name in tensor_classes and d["flops"] > 0:
+            r.update(achieved=d["flops"] / (d["ms"] / 1e3) / 1e12, unit="TFLOP/s", peak=peak_tc)
+        elif name in hbm_classes and d["bytes"] > 0:
+            r.update(achieved=d["bytes"] / (d["ms"] / 1e3) / 1e9, unit="GB/s", peak=hbm)
+        if "achieved" in r:
+            r["frac"] = r["achieved"] / r["peak"]
+        kern[name] = r
+    dom = max((k for k in kern if "achieved" in kern[k]), key=lambda k: kern[k]["ms"])
+    dk = kern[dom]
+    roof = {"bound": "tensor" if dom in tensor_classes else "hbm", "achieved": dk["achieved"], "peak": dk["peak"],
+            "unit": dk["unit"], "frac": dk["frac"], "traffic": None, "kernel": dom, "share_of_step": dk["share_of_step"],
+            "peak_note": tc_note if dom in tensor_classes else f"{peak_src} HBM copy bandwidth (read + write bytes)",
+            "achieved_note": "algorithmic flops (8 M per step, R13) or bytes (DESIGN.md Kernels) of every launch of "
+                             "this kernel class / its summed CUDA-event time on the launching stream"}
+    tr = load_traffic(ci)
+    if tr and tr.get("kernel") == dom:
+        roof["traffic"] = tr["dram_bytes"]
+        roof["traffic_probe"] = tr
     clocks = clk.summary()
     if roof["bound"] == "tensor" and dtype == tb.TN_C64 and clocks.get("sm_mhz"):
         # the measured cuBLAS "sustained" denominator ran at its own power-capped clock; the
         # tensor pipe's own ceiling at this run's median clock: a 128 x 128 x 16 tcgen05 MMA
         # every 64 cycles per SM (8192 fp16 flops / clk / SM), 24 fp16 flops per useful 8
         at_clk = 8192.0 * 148 * clocks["sm_mhz"] * 1e6 / 1e12 / F16_FLOPS_PER_USEFUL
-        roof["clock_ceiling"] = {"sm_mhz": clocks["sm_mhz"], "useful_tflops": at_clk, "frac": gemm_tfs / at_clk,
+        roof["clock_ceiling"] = {"sm_mhz": clocks["sm_mhz"], "useful_tflops": at_clk, "frac": roof["achieved"] / at_clk,
                                  "note": "8192 fp16 flops/clk/SM (tcgen05 m128n128k16 floor of 64 cycles) x 148 SMs "
                                          "x median SM clock of the timed region / 3"}
-    if by_slices:
-        step_desc = (f"one slice (of 2^{slice_bits}) of one amplitude; rank r takes slices [rK, (r+1)K), "
-                     "partial amplitudes summed by one NCCL all-reduce in the timed region")
-    elif n_slices > 1:
-        step_desc = f"one slice (of {n_slices}) of one amplitude; rank r takes bitstrings r::N of {len(bits)}"
-    else:
-        step_desc = f"one full amplitude (unsliced); rank r takes bitstrings r::N of {len(bits)}"
-    prec = "block-scaled fp16x2 split on tcgen05" if dtype == tb.TN_C64 else "FP64 tensor pipe (DMMA)"
     line = {
-        "metric": METRIC, "value": value, "unit": "FLOP/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": "FLOP/s", "n_gpus": ws, "steps": K,
+        "warmup": W, "ms_per_step": ms / max(steps_mine, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": spec["dtype"], "data": "synthetic",
-        "config": {"workload": workload_name(ci, c, slice_log2),
-                   "step": step_desc, "flops_per_step": flops_step,
-                   "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice if flops_slice else None,
-                   "slice_bits": slice_bits, "contributing_slices": contrib,
-                   "l2": "working set (GB intermediates) >> 126 MB L2, no flush" if pinfo["arena_bytes"] > 1e9
-                         else "arena below L2 size: steps re-read warm intermediates (no flush)",
-                   "arena_gb": pinfo["arena_bytes"] / 1e9},
+        "config": shared_config(ci, c, len(bits), slice_bits, flops_slice),
+        "arithmetic": ("complex64 on block-scaled fp16x2 split-precision tcgen05 tensor cores (fp32 accumulation), "
+                       "CUDA-core fp32 for skinny / wide steps" if dtype == tb.TN_C64 else
+                       "complex128 on the FP64 tensor pipe (DMMA) and fp64 CUDA cores"),
         "amplitudes_per_s": amps_per_s,
+        "contributing_slices_mean": contrib_mean,
         "amplitudes_per_s_lanes": lanes_line,
+        "slicing": {"slice_bits": slice_bits, "log2_sliced_work": oinfo["log2_slice_2M"] - 1.0 + slice_bits,
+                    "log2_unsliced_work": oinfo["log2_total_2M"] - 1.0,
+                    "note": "Eq. (3) multiplications sum_k M_k of the whole amplitude: all slices vs the unsliced "
+                            "order (the slicing overhead)",
+                    "ssa_splits_median_fallbacks": oinfo["median_fallbacks"]},
+        "plan": {"arena_gb": pinfo["arena_bytes"] / 1e9, "tc_flops_fraction": pinfo["tc_flops_per_slice"] / flops_slice,
+                 "launches_per_slice": pinfo["n_launches_per_slice"]},
         "roofline": roof,
-        "kernel_ms": {k: prof[k] for k in ("ms_gemm", "ms_pack", "ms_small", "ms_other")},
-        "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(nq),
-                "d2h_bytes_per_step": 16},
+        "kernels": kern,
+        "check": {"steps": n_chk, "max_rel_diff_vs_graph_path": rel},
+        "e2e": {"value": e2e_value, "unit": "FLOP/s", "h2d_bytes_per_step": int(c.n), "d2h_bytes_per_step": 16},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and ws == 1:      # the oracle baseline: rank 0 at N = 1 only
-        line["cpu_baseline"] = cpu_baseline_sample(c, bits, order.steps(), order.slices(), budget_s=args.cpu_budget,
+        line["cpu_baseline"] = cpu_baseline_sample(c, bits, oracle_order(ci), budget_s=args.cpu_budget,
                                                    hyper=spec["hyper"])
     print(json.dumps(line))
     if distributed:

@@ -175,11 +175,23 @@ int tn_contract_device(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begi
 /* tn_contract_profiled: as tn_contract_device, but launches eagerly (no graph) with
  * CUDA events around every launch on `stream`; prof (host) receives the summed
  * device time per kernel class and the algorithmic flops of the GEMM launches. */
+/* kernel classes of tn_profile.k_*: small-path waves, fp16x2 tensor-core pack, the
+ * complex64 tcgen05 GEMMs (single-CTA cgemm_f16x2s_kernel, one-tile-per-pair
+ * cgemm2_f16x2s_kernel, persistent pair cgemm2p_f16x2s_kernel), planar pack (skinny /
+ * wide / DMMA operands), complex128 DMMA GEMM, skinny, wide, split-K reductions, other */
+enum {
+  TN_K_SMALL = 0, TN_K_PACK_TC, TN_K_GEMM_SINGLE, TN_K_GEMM_PAIR, TN_K_GEMM_PERSIST, TN_K_PACK_PLANAR,
+  TN_K_DMMA, TN_K_SKINNY, TN_K_WIDE, TN_K_REDUCE, TN_K_OTHER, TN_K_COUNT
+};
 typedef struct {
   double ms_small, ms_pack, ms_gemm, ms_other;
   double flops_gemm, flops_small;          /* 8 * M (real flops of the complex MACs) */
   double bytes_small, bytes_pack;          /* algorithmic bytes read + written */
   int64_t n_gemm, n_pack, n_small, n_other;
+  /* per kernel class (TN_K_*): device ms between its events, algorithmic flops and
+   * bytes, number of timed intervals */
+  double k_ms[16], k_flops[16], k_bytes[16];
+  int64_t k_intervals[16];
 } tn_profile;
 int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end,
                          void* amp_dev, void* stream, tn_profile* prof);

@@ -456,26 +456,34 @@ def _build(ctx, ids, sid, depth):
     return _merge(ctx, nE, nI)
 
 
+def _one_hierarchy(args):
+    """One randomized hierarchy (root stream 1 + r) and its R10 objective."""
+    net, seed, leaf_size, a_max, n_valid, max_tries, max_log2_size, r = args
+    ctx = _Ctx(net, seed, leaf_size, a_max, n_valid, max_tries)
+    ids = list(range(len(net.tensors)))
+    _build(ctx, ids, 1 + r, 0)
+    tot = 0.0
+    for m, _ in step_costs(net, ctx.steps):
+        tot = tot + 2.0 ** (m + 1)
+    if max_log2_size > 0:
+        tot = sliced_work(net, ctx.steps, choose_slices(net, ctx.steps, max_log2_size))
+    return tot, ctx.steps, ctx.log
+
+
 def find_order(net, seed: int = 0, leaf_size: int = 8, a_max: int = 32, n_valid: int = 64,
-               max_tries: int = 256, n_seeds: int = 4, max_log2_size: int = 0):
+               max_tries: int = 256, n_seeds: int = 4, max_log2_size: int = 0, map_fn=map):
     """Separator hierarchy (Fig. 2) -> list of pairwise steps (a, b); leaves are
     tensor ids 0..n-1, step k creates node id n + k.  Post-order: E subtree, I
     subtree, then their merge.  The randomized hierarchy is built n_seeds times
     (root stream ids 1..n_seeds) and the one with the smallest Eq. (3) total
     sum_k 2 M_k is kept -- with a slicing target, the smallest total of all slices,
-    sliced_work(choose_slices(...)) (R10; ties -> earliest)."""
+    sliced_work(choose_slices(...)) (R10; ties -> earliest).  The hierarchies are
+    independent; `map_fn` (e.g. a process pool's map, order-preserving) builds them."""
     best = None
-    for r in range(n_seeds):
-        ctx = _Ctx(net, seed, leaf_size, a_max, n_valid, max_tries)
-        ids = list(range(len(net.tensors)))
-        _build(ctx, ids, 1 + r, 0)
-        tot = 0.0
-        for m, _ in step_costs(net, ctx.steps):
-            tot = tot + 2.0 ** (m + 1)
-        if max_log2_size > 0:
-            tot = sliced_work(net, ctx.steps, choose_slices(net, ctx.steps, max_log2_size))
+    args = [(net, seed, leaf_size, a_max, n_valid, max_tries, max_log2_size, r) for r in range(n_seeds)]
+    for tot, steps, log in map_fn(_one_hierarchy, args):
         if best is None or tot < best[0]:
-            best = (tot, ctx.steps, ctx.log)
+            best = (tot, steps, log)
     return best[1], best[2]
 
 

@@ -46,7 +46,15 @@ class Profile(C.Structure):
     _fields_ = [("ms_small", C.c_double), ("ms_pack", C.c_double), ("ms_gemm", C.c_double),
                 ("ms_other", C.c_double), ("flops_gemm", C.c_double), ("flops_small", C.c_double),
                 ("bytes_small", C.c_double), ("bytes_pack", C.c_double), ("n_gemm", C.c_int64),
-                ("n_pack", C.c_int64), ("n_small", C.c_int64), ("n_other", C.c_int64)]
+                ("n_pack", C.c_int64), ("n_small", C.c_int64), ("n_other", C.c_int64),
+                ("k_ms", C.c_double * 16), ("k_flops", C.c_double * 16), ("k_bytes", C.c_double * 16),
+                ("k_intervals", C.c_int64 * 16)]
+
+
+# kernel classes of Profile.k_* (include/tn.h TN_K_*)
+KERNEL_CLASSES = ["small_contract_kernel", "pack_f16x2s_kernel", "cgemm_f16x2s_kernel", "cgemm2_f16x2s_kernel",
+                  "cgemm2p_f16x2s_kernel", "pack_planar_kernel", "zgemm_dmma_kernel", "skinny_kernel",
+                  "wide_kernel", "reduce (splitk / skinny)", "other"]
 
 
 class _PlanInfo(C.Structure):
@@ -261,7 +269,11 @@ class Plan:
         pr = Profile()
         _check(lib.tn_contract_profiled(self.h, C.c_void_p(bits_dev_ptr), int(slice_begin), int(slice_end),
                                         C.c_void_p(amp_dev_ptr), C.c_void_p(stream), C.byref(pr)))
-        return {k: getattr(pr, k) for k, _ in pr._fields_}
+        out = {k: getattr(pr, k) for k, _ in pr._fields_ if not k.startswith("k_")}
+        out["kernels"] = {name: {"ms": pr.k_ms[i], "flops": pr.k_flops[i], "bytes": pr.k_bytes[i],
+                                 "intervals": int(pr.k_intervals[i])}
+                          for i, name in enumerate(KERNEL_CLASSES)}
+        return out
 
     def amplitudes(self, bits, stream=None):
         b = np.ascontiguousarray(bits, dtype=np.uint8)

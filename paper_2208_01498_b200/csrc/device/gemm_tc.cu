@@ -8,7 +8,7 @@
 // is scaled by a power of two per (row, 128-element K chunk) so the chunk maximum lies
 // just below 2^14, then split into two fp16 pieces x = x0 + x1 (x0 = fp16(x),
 // x1 = fp16(x - x0)): 22 significand bits, the representation error is
-// <= 2^-24 |x| + 2^-39 max|chunk|.  The three products x0 y0, x0 y1, x1 y0 are
+// <= 2^-24 |x| + 2^-38 max|chunk|.  The three products x0 y0, x0 y1, x1 y0 are
 // accumulated in fp32 on tcgen05 (kind::f16, fp16 inputs, fp32 accumulators in TMEM);
 // the dropped x1 y1 is <= 2^-24 |x y|.  That is fp32-level accuracy at 3 MMAs per real
 // product (bf16x3 splitting needs 6).  Complex arithmetic is planar:
@@ -33,7 +33,7 @@ namespace tnd {
 // The operand's stored order and the matricised order [b][rows][k] are both
 // row-major over power-of-two dimensions, so the permutation is a permutation of the
 // bits of the element index.  One CTA handles a tile of 2^t_bits elements whose bits
-// T contain the source's 5 lowest bits (coalesced 256-byte reads) and the
+// T contain the source's 4 lowest bits (coalesced 128-byte reads of complex64) and the
 // destination's lowest bits (coalesced 16-byte writes); the tile is transposed
 // through shared memory.
 struct PackDesc {
@@ -63,8 +63,14 @@ __device__ __forceinline__ int pack_slot(int q) { return q ^ ((((q >> 4) ^ (q >>
 // elements of one row (re and im together) gets a power-of-two scale 2^(e-14), e the
 // exponent with max|x| < 2^e, so the scaled chunk lies in (-2^14, 2^14): the top of the
 // fp16 range, which keeps the second piece of elements far below the chunk maximum out
-// of the fp16 subnormals (absolute floor 2^-25 * 2^-14 of the chunk maximum).
+// of the fp16 subnormals (absolute error floor 2^-25 in the scaled unit, i.e. at most
+// 2^-38 of the chunk maximum, which is >= 2^13 after scaling).
 constexpr int SCALE_LOG2 = 7;   // 128-element K chunks = 4 GEMM stages per TMEM promotion
+// a chunk (2^SCALE_LOG2 destination elements, 8 per thread) must lie within one warp for
+// the shuffle max, and the tile must hold the chunk's destination bits plus the 4 lowest
+// source bits (make_pack)
+static_assert(SCALE_LOG2 <= 3 + 5, "scale chunk wider than one warp of pack threads");
+static_assert(SCALE_LOG2 + 4 <= PACK_MAX_T, "pack tile too small for a scale chunk plus 4 source bits");
 
 // split two scaled floats into two fp16x2 pieces: hi = fp16(x), lo = fp16(x - hi)
 __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_t& p1) {
@@ -77,8 +83,8 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 
 // out planes, layout [b][4][r][k] fp16, plane = 2 * piece + {0: re, 1: im}; scales
 // [b][K / 128][r] fp32 (one per row and 128-element K chunk; one per row if K < 128).
-// Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..5 always
-// inside the tile, so every K chunk is held by 2, 4 or 8 adjacent threads of one warp.
+// Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..6 always
+// inside the tile, so every K chunk is held by 2-16 adjacent threads of one warp.
 __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
@@ -163,6 +169,23 @@ namespace tc {
 constexpr int BM = 128;    // rows per tile (TMEM lanes)
 constexpr int BK = 32;     // fp16 elements of K per smem stage (64-byte rows, SWIZZLE_64B)
 constexpr int PROMO = 4;   // stages per TMEM accumulation = one 128-element scale chunk
+
+// Debiasing of the truncating TMEM accumulation: tcgen05
+// adds each MMA's products to the fp32 accumulator rounding toward zero, so a chunk sum
+// built by T MMA updates comes out shrunk by ~beta(T) 2^-24 of itself -- coherently,
+// and the amplitude is multilinear in every step's result, so the shrinks of all
+// tensor-core steps multiply (measured 3-4e-5 on one configs[1] slice without this).
+// beta measured on dense random operands (scripts/diag_bias2.py; Gaussian / unit-phase /
+// log-normal: T = 6, 12, 24, 48 -> 3.1, 4.7, 8.0, 13-14.6; 70%-sparse: 2.6 .. 10.8).  The
+// promotion scales the chunk by 1 + beta 2^-24 with beta rounded to an even number of
+// units, so the factor is exact in fp32 and the per-chunk power-of-two scale stays exact.
+// T = 12 MMA updates per 32-element stage of K (2 k16 blocks x 3 fp16x2 products x 2
+// complex terms); 6 when K = 16 (half a stage).
+__device__ __forceinline__ float rz_debias(int stages, int K) {
+  const int T = K < BK ? 6 : 12 * stages;
+  const int beta = T >= 48 ? 14 : T >= 36 ? 12 : T >= 24 ? 8 : T >= 12 ? 4 : 2;
+  return 1.0f + (float)(beta >> 1) * 0x1p-23f;
+}
 // CTA rasterization: GROUP_M M-tiles sweep the N tiles together (panels shared in L2).
 // Measured with scripts/raster_sweep.sh (DRAM traffic costs clock under the power cap):
 // pair kernel 4 (DRAM reads 67 -> 55 GB on a (2^18, 2^12, 2^12) step, 1-2% faster);
@@ -344,7 +367,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 constexpr int EPI_PITCH = 132;   // floats per staged C row (64 complex + 16 B pad: conflict-free)
 template <int BN, bool kPair>
 __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, uint32_t tmem, const float* sc, uint64_t* sfull,
-                                         uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int n_promo,
+                                         uint64_t* sempty, uint64_t* tfull, uint64_t* tempty, int nk, int K,
                                          float2* C, int b, int M, int N, int row0, int col0_blk, bool acc_c,
                                          int c_rows, int c_row_off, const CUtensorMap* tmC = nullptr) {
   using CF = Cfg<BN>;
@@ -354,13 +377,14 @@ __device__ __forceinline__ void epilogue(float* stage_smem, int warp, int lane, 
   float ar[64], ai[64];
 #pragma unroll
   for (int j = 0; j < 64; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
+  const int n_promo = (nk + PROMO - 1) / PROMO;
   for (int pi = 0; pi < n_promo; ++pi) {
     const int buf = pi & 1, slot = pi % CF::SLOTS;
     mbar_wait(&sfull[slot], (pi / CF::SLOTS) & 1);
     mbar_wait(&tfull[buf], (pi >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t scs = smem_u32(sc + slot * (BM + BN));
-    const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
+    const float sa = lds_f32(scs + 4 * (lg * 32 + lane)) * rz_debias(min(PROMO, nk - pi * PROMO), K);
     // column scales: one conflict-free load per lane, broadcast by shuffles (broadcast
     // LDS.128s cost 4 shared wavefronts each, competing with the MMA operand reads)
     const float sb_lo = lds_f32(scs + 4 * (BM + ch * 64 + lane));
@@ -562,7 +586,6 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   const int kc0 = split * kc_per_split;
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
   const int nch_all = (nk_all + PROMO - 1) / PROMO;     // scale chunks of the whole K
-  const int n_promo = (nk + PROMO - 1) / PROMO;
 
   if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -613,7 +636,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   } else {
     // ---- epilogue warps: promote every stage, scaled, into fp32 registers ----
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
-    epilogue<BN, false>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, m_blk * BM,
+    epilogue<BN, false>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, nk, K, C, b, M, N, m_blk * BM,
                         n_blk * BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -724,7 +747,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
   const int kc0 = k_base + split * kc_per_split;     // k_base: K-chunk of a long-K step (stages)
   const int nk = min(nk_all, kc0 + kc_per_split) - kc0;
   const int nch_all = (nk_all + PROMO - 1) / PROMO;
-  const int n_promo = (nk + PROMO - 1) / PROMO;
 
   if (warp == TMA_WARP && lane == 0) {
     for (int s = 0; s < CF::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -775,7 +797,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
     }
   } else {
     float2* C = partial ? partial + (int64_t)split * nb * M * (int64_t)N : reinterpret_cast<float2*>(ptrs[c_node]);
-    epilogue<128, true>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, n_promo, C, b, M, N, row0,
+    epilogue<128, true>(reinterpret_cast<float*>(smem), warp, lane, tmem, sc, sfull, sempty, tfull, tempty, nk, K, C, b, M, N, row0,
                         n_blk * CF::BN, accumulate && !partial, partial ? M : M_c, partial ? 0 : m_off,
                         partial ? nullptr : &tmC);
   }
@@ -979,7 +1001,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::THREADS, 1)
         mbar_wait(&tfull[buf], (gp >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t scs = smem_u32(sc + slot * (BM + CF::BN));
-        const float sa = lds_f32(scs + 4 * (lg * 32 + lane));
+        const float sa = lds_f32(scs + 4 * (lg * 32 + lane)) * rz_debias(min(PROMO, nk - p * PROMO), K);
         const float sb_lo = lds_f32(scs + 4 * (BM + ch * 64 + lane));
         const float sb_hi = lds_f32(scs + 4 * (BM + ch * 64 + 32 + lane));
         const uint32_t t_re = tmem + buf * CF::ACC_COLS + lane_base + ch * 64, t_im = t_re + CF::BN;

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <set>
 #include <stdexcept>
@@ -193,14 +194,22 @@ CUtensorMap make_c_map(void* base, int n_bits, int64_t rows) {
   return m;
 }
 
+// The dynamic shared memory limit is a per-device function attribute: set it once per
+// (kernel, current device), under a lock (plans may live on several devices / threads).
+void ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({fn, dev})) return;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({fn, dev});
+}
+
 template <int BN>
 void ensure_gemm_attr() {
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute(tnd::tc::cgemm_f16x2s_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            tnd::tc::Cfg<BN>::SMEM));
-    done = true;
-  }
+  ensure_smem_attr((const void*)tnd::tc::cgemm_f16x2s_kernel<BN>, tnd::tc::Cfg<BN>::SMEM);
 }
 
 // one tensor-core step: pack X, pack Y, GEMM
@@ -233,15 +242,18 @@ struct TcStep {
 };
 
 // profiling marks: an event recorded before each kernel class (0 small, 1 pack, 2 gemm,
-// 3 reduce, 4 other); time between consecutive marks is attributed to the earlier one
+// 3 reduce, 4 other) and its kernel (TN_K_*, tn_profile.k_*); time between consecutive
+// marks is attributed to the earlier one
 struct Marks {
   std::vector<std::pair<cudaEvent_t, int>> v;
+  std::vector<int> fine;
   std::vector<std::string> tags;
-  void mark(cudaStream_t st, int cat, std::string tag = "") {
+  void mark(cudaStream_t st, int cat, int k, std::string tag = "") {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     CK(cudaEventRecord(e, st));
     v.push_back({e, cat});
+    fine.push_back(k);
     tags.push_back(std::move(tag));
   }
 };
@@ -277,24 +289,25 @@ bool uses_persist(const TcStep& t) {
   return t.kind == K_TC && t.pair && gemm_persist_enabled() && stages_per_tile <= max_stages;
 }
 
+// kernel class (TN_K_*) of a complex64 tensor-core step's GEMM launches
+int gemm_class(const TcStep& t) {
+  return uses_persist(t) ? TN_K_GEMM_PERSIST : t.pair ? TN_K_GEMM_PAIR : TN_K_GEMM_SINGLE;
+}
+
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
 int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_bits + d.k_bits); }
 
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                  Marks* mk) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(tnd::zg::zgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tnd::zg::SMEM));
-    attr = true;
-  }
-  if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("f64 pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+  ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_kernel, tnd::zg::SMEM);
+  if (mk) mk->mark(st, 1, TN_K_PACK_PLANAR, profile_dump_ms() >= 0 ? shape_tag("f64 pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   for (const PackDesc* d : {&t.px, &t.py}) {
     const int64_t blocks = std::min<int64_t>(int64_t(1) << d->tile_bits, 148 * 8);
     tnd::pack_planar_kernel<double><<<(unsigned)blocks, tnd::PACK_THREADS, 0, st>>>(
         ptrs_d, *d, tab_d, reinterpret_cast<double*>(arena + (d == &t.px ? t.x_off : t.y_off)), 0);
     g_launches++;
   }
-  if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("dmma", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+  if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
                         (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
@@ -326,10 +339,11 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
   const R* Y = reinterpret_cast<const R*>(arena + t.y_off);
   const bool dump = profile_dump_ms() >= 0;
   for (int s = 0; s < t.n_slabs; ++s) {
-    if (mk) mk->mark(st, 1, dump ? shape_tag("planar pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    if (mk) mk->mark(st, 1, TN_K_PACK_PLANAR, dump ? shape_tag("planar pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
     pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
-    if (mk) mk->mark(st, 0, dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
+    if (mk) mk->mark(st, 0, t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE,
+                     dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
                                              t.k_bits) : "");
     if (t.kind == K_SKINNY) {
       const int64_t K = int64_t(1) << t.k_lo;
@@ -348,7 +362,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
 #undef TN_SKINNY
       g_launches++;
       if (t.S * ws == 1) continue;      // the kernel wrote C
-      if (mk) mk->mark(st, 3);
+      if (mk) mk->mark(st, 3, TN_K_REDUCE);
       const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
       tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
           partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
@@ -409,33 +423,23 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
   // row slabs (outer) or K-slabs (inner); at most one of them has more than one slab
   for (int ms = 0; ms < t.n_mslabs; ++ms)
   for (int s = 0; s < t.n_slabs; ++s) {
-    if (mk) mk->mark(st, 1, profile_dump_ms() >= 0 ? shape_tag("pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    if (mk) mk->mark(st, 1, TN_K_PACK_TC, profile_dump_ms() >= 0 ? shape_tag("pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[t.n_mslabs > 1 ? ms : s]);
     if (ms == 0) pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
-    if (mk) mk->mark(st, 2, profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    if (mk) mk->mark(st, 2, gemm_class(t), profile_dump_ms() >= 0 ? shape_tag("gemm", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
     const int acc = s > 0;
     const int m_off = ms << t.m_lo;
     // persistent tile loop only for short K per tile (<= 32 stages): there the per-CTA
     // prologue / fill / drain is a large share; long tiles are faster one per CTA pair
     if (uses_persist(t)) {
-      static bool attr2p = false;
-      if (!attr2p) {
-        CK(cudaFuncSetAttribute(tnd::tc::cgemm2p_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tnd::tc::Cfg2P::SMEM));
-        attr2p = true;
-      }
+      ensure_smem_attr((const void*)tnd::tc::cgemm2p_f16x2s_kernel, tnd::tc::Cfg2P::SMEM);
       const int64_t tiles = (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7)) * (int64_t(1) << t.nb_bits) * t.S;
       const int64_t n_pairs = std::min<int64_t>(tiles, 74);
       tnd::tc::cgemm2p_f16x2s_kernel<<<(unsigned)(2 * n_pairs), tnd::tc::Cfg2::THREADS, tnd::tc::Cfg2P::SMEM, st>>>(
           t.ta, t.tb, sca, scb, ptrs_d, t.c_node, 1 << t.m_lo, 1 << t.n_bits, 1 << t.k_lo, 1 << t.nb_bits, t.S,
           t.kc_split, partial, acc, m_off, 1 << t.m_bits, t.tc);
     } else if (t.pair) {
-      static bool attr2 = false;
-      if (!attr2) {
-        CK(cudaFuncSetAttribute(tnd::tc::cgemm2_f16x2s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tnd::tc::Cfg2::SMEM));
-        attr2 = true;
-      }
+      ensure_smem_attr((const void*)tnd::tc::cgemm2_f16x2s_kernel, tnd::tc::Cfg2::SMEM);
       const int64_t pairs = (int64_t(1) << (t.m_lo - 8)) * (int64_t(1) << (t.n_bits - 7));
       dim3 grid2((unsigned)(2 * pairs), 1, (unsigned)((1u << t.nb_bits) * t.S));
       for (int ch = 0; ch < t.n_kchunks; ++ch) {
@@ -457,7 +461,7 @@ void launch_tc(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t*
     }
     g_launches++;
     if (t.S > 1) {
-      if (mk) mk->mark(st, 3);
+      if (mk) mk->mark(st, 3, TN_K_REDUCE);
       const int64_t n = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
       const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
       tnd::splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(partial, t.S, n, ptrs_d, t.c_node, acc);
@@ -650,6 +654,9 @@ PackDesc make_pack(TabPool& pool, int src_node, const NodeLayout& L, const std::
   int ld = 0;
   while (ld < D && inT[ld]) ++ld;
   d.ld = std::min(ld, RK);
+  // the pack kernels write 8 consecutive destination elements per thread: a (batch, row)
+  // block of the destination must hold >= 8 contiguous entries (rows + K bits >= 3)
+  if (d.ld < 3) throw Err(TN_EUNSUPPORTED, "pack: an operand needs rows + K >= 8 entries per batch");
   std::vector<int> Tsrc, Tdst, nonT;
   for (int j = 0; j < D; ++j) (inT[j] ? Tdst : nonT).push_back(j);
   Tsrc = Tdst;
@@ -713,7 +720,8 @@ bool want_skinny(int nb, int m, int n, int k) {
   return (k >= 10 || (k >= 6 && nb >= 6)) && m <= 6 && n <= 6 && m + n <= 8 && nb <= 15 && (nb + m + n + k) >= 20;
 }
 bool want_wide(int nb, int m, int n, int k) {
-  return k <= 4 && (nb + m + n) >= 18 && nb <= 24 && (nb + m + k) >= 3 && (nb + n + k) >= 3;
+  // each planar operand needs >= 8 entries per batch (rows + K bits >= 3, see make_pack)
+  return k <= 4 && (nb + m + n) >= 18 && nb <= 24 && (m + k) >= 3 && (n + k) >= 3;
 }
 void finish_tc_kind(TcStep& t, int dtype) {
   t.kind = dtype == TN_C128 ? K_DMMA : K_TC;
@@ -1317,7 +1325,7 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
   std::memset(&pr, 0, sizeof(pr));
   for (int64_t s = s0; s < s1; ++s) {
     Marks mk;
-    mk.mark(st, 4);
+    mk.mark(st, 4, TN_K_OTHER);
     tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
         P.ptrs_d, P.leaf_base_d, P.var_begin_d, P.var_kind_d, P.var_stride_d, P.n_leaves, P.bits_d, P.slice_d,
         P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
@@ -1333,7 +1341,7 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
             if (x.nb_bits + x.m_bits + x.n_bits + x.k_bits > y.nb_bits + y.m_bits + y.n_bits + y.k_bits) big = q;
           }
           const auto& d = w.steps[big];
-          mk.mark(st, 0, profile_dump_ms() >= 0 ? shape_tag(("wave of " + std::to_string(w.steps.size()) + ", largest").c_str(),
+          mk.mark(st, 0, TN_K_SMALL, profile_dump_ms() >= 0 ? shape_tag(("wave of " + std::to_string(w.steps.size()) + ", largest").c_str(),
                                                            d.nb_bits, d.m_bits, d.n_bits, d.k_bits) : "");
         }
         if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
@@ -1341,36 +1349,53 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
         pr.n_small++;
         pr.flops_small += P.waves[L.second].flops;
         pr.bytes_small += P.waves[L.second].bytes;
+        pr.k_flops[TN_K_SMALL] += P.waves[L.second].flops;
+        pr.k_bytes[TN_K_SMALL] += P.waves[L.second].bytes;
       } else {
         const auto& t = P.tcs[L.second];
         launch_tc(t, P.arena, P.ptrs_d, P.tab_d, st, &mk);
         const double ex = std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits), ey = std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits);
         pr.n_pack += 2 * t.n_slabs;
+        // algorithmic bytes: a planar pack reads and writes every entry once (2 esz per
+        // entry); the fp16x2 pack reads 8 and writes 8 bytes per entry plus one fp32
+        // scale per 128-entry K chunk; skinny / wide read both planar operands and write C
         if (t.kind == K_SKINNY || t.kind == K_WIDE) {   // CUDA-core: accounted with the small path
+          const double b = t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
           pr.n_small += t.n_slabs;
           pr.flops_small += t.flops;
-          pr.bytes_small += t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
+          pr.bytes_small += b;
           pr.bytes_pack += 2.0 * t.esz * (ex + ey);
+          const int kc = t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE;
+          pr.k_flops[kc] += t.flops;
+          pr.k_bytes[kc] += b;
+          pr.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
         } else {
+          const double pb = (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
           pr.n_gemm += t.n_slabs * t.n_mslabs;
           pr.n_pack += t.n_mslabs - 1;
           pr.flops_gemm += t.flops;
-          pr.bytes_pack += (t.kind == K_DMMA ? 32.0 : 16.125) * (ex + ey);
+          pr.bytes_pack += pb;
+          pr.k_flops[t.kind == K_DMMA ? TN_K_DMMA : gemm_class(t)] += t.flops;
+          pr.k_bytes[t.kind == K_DMMA ? TN_K_PACK_PLANAR : TN_K_PACK_TC] += pb;
         }
       }
     }
-    mk.mark(st, 4);
+    mk.mark(st, 4, TN_K_OTHER);
     if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
     else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
     g_launches++;
     pr.n_other++;
-    mk.mark(st, -1);
+    mk.mark(st, -1, TN_K_OTHER);
     CK(cudaEventSynchronize(mk.v.back().first));
     for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, mk.v[j].first, mk.v[j + 1].first));
       if (profile_dump_ms() >= 0 && ms > profile_dump_ms())
         fprintf(stderr, "[tn profile] %8.3f ms  cat %d  %s\n", ms, mk.v[j].second, mk.tags[j].c_str());
+      if (mk.fine[j] >= 0 && mk.fine[j] < TN_K_COUNT) {
+        pr.k_ms[mk.fine[j]] += ms;
+        pr.k_intervals[mk.fine[j]]++;
+      }
       switch (mk.v[j].second) {
         case 0: pr.ms_small += ms; break;
         case 1: pr.ms_pack += ms; break;
@@ -1799,8 +1824,8 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
     if (big == K_DMMA && kk < 1) throw Err(TN_EUNSUPPORTED, "DMMA path needs K >= 2 (complex128)");
     if (big == K_SKINNY && (mx > 6 || my > 6 || mx + my > 8 || kk < 1 || nb > 15))
       throw Err(TN_EUNSUPPORTED, "skinny path needs M, N <= 64, M N <= 256, K >= 2");
-    if (big == K_WIDE && (kk > 4 || nb + mx + kk < 3 || nb + my + kk < 3))
-      throw Err(TN_EUNSUPPORTED, "wide path needs K <= 16 and >= 8 entries per operand");
+    if (big == K_WIDE && (kk > 4 || mx + kk < 3 || my + kk < 3))
+      throw Err(TN_EUNSUPPORTED, "wide path needs K <= 16 and >= 8 entries per operand and batch");
     cudaStream_t st = (cudaStream_t)stream;
     int cur = 0;
     CK(cudaGetDevice(&cur));

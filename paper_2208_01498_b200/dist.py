@@ -1,13 +1,16 @@
 """Multi-GPU partitioning of the contraction (one process per GPU, torch.distributed).
 
 Two ways the path shards (BASELINE north_star "Index slicing and multi-GPU
-partitioning"):
+partitioning"); both are used by bench.py and by the tests, so the code that would run
+on 8 GPUs is the code the tests run:
   * bitstrings: independent amplitudes -> contiguous blocks of the batch per rank, no
-    data-path collective (an all_gather only returns the results to every rank);
+    data-path collective;
   * slices: the sliced sub-contractions of ONE amplitude ("index
-    slicing") are independent -> contiguous slice ranges per rank, the partial
-    amplitudes are summed with ONE all-reduce (NCCL over NVLink on the GPU path).
-The contraction itself is a callable so the host logic is testable with gloo on CPU.
+    slicing") are independent -> disjoint contiguous blocks of its (contributing)
+    slices per rank, the partial amplitudes summed with ONE all-reduce (NCCL over
+    NVLink on the GPU path, gloo in the CPU tests).
+Every function takes the world size / rank explicitly or from the default process
+group; nothing here does contraction arithmetic.
 """
 from __future__ import annotations
 
@@ -15,40 +18,86 @@ import torch
 import torch.distributed as dist
 
 
+def world_rank(group=None):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
 def block_range(n: int, world: int, rank: int):
-    """Contiguous, balanced block [lo, hi) of n items for `rank`."""
+    """Contiguous, balanced block [lo, hi) of n items for `rank` (blocks of all ranks are
+    disjoint and cover [0, n); sizes differ by at most one)."""
     q, r = divmod(n, world)
     lo = rank * q + min(rank, r)
     return lo, lo + q + (1 if rank < r else 0)
 
 
+def slice_block(live_slices, world: int, rank: int):
+    """This rank's block of the slices of one amplitude: `live_slices` is the list of
+    slice ids to contract (the contributing ones, tn_contributing_slice_ids), the ranks
+    get disjoint contiguous blocks, so the all-reduced sum counts every slice once."""
+    lo, hi = block_range(len(live_slices), world, rank)
+    return list(live_slices[lo:hi])
+
+
+def bitstring_steps(contributing_ids, rows, count: int):
+    """Work items (row, slice) for `count` steps over this rank's bitstrings `rows`
+    (indices into the batch), one contributing slice per step, bitstring by bitstring:
+    contributing_ids(row, n) -> the first n contributing slice ids of that bitstring.
+    No (row, slice) pair repeats; fewer than `count` items if the rows run out."""
+    items = []
+    for r in rows:
+        if len(items) >= count:
+            break
+        for s in contributing_ids(r, count - len(items)):
+            items.append((r, s))
+    return items
+
+
+def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM over ranks (the one data-path collective of the sliced path);
+    a no-op without a process group / at world size 1."""
+    w, _ = world_rank(group)
+    if w > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def max_over_ranks(x: float, device=None, group=None) -> float:
+    """max of a host float over ranks (timings are the max over ranks)."""
+    w, _ = world_rank(group)
+    if w == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 def sliced_amplitude(contract_range, n_slices: int, group=None, device=None) -> complex:
     """sum_{s} contract(s) over all slices, each rank contracting its block of slices
     (contract_range(lo, hi) -> complex partial sum), summed by one all-reduce."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world, rank = world_rank(group)
     lo, hi = block_range(n_slices, world, rank)
     part = contract_range(lo, hi) if hi > lo else 0j
     if world == 1:
         return complex(part)
     t = torch.tensor([part.real, part.imag], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    allreduce_sum_(t, group)
     return complex(t[0].item(), t[1].item())
 
 
 def amplitudes_by_bitstring(contract_one, bits, group=None, device=None):
     """Amplitudes of all bitstrings; rank r contracts its contiguous block
-    (contract_one(bitstring) -> complex).  Results are all-gathered (not a data-path
-    collective: every amplitude is computed by exactly one rank)."""
+    (contract_one(bitstring) -> complex).  Results are gathered by an all-reduce of
+    disjoint supports (not a data-path collective: every amplitude is computed by
+    exactly one rank)."""
     n = len(bits)
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world, rank = world_rank(group)
     lo, hi = block_range(n, world, rank)
     mine = torch.zeros(2 * n, dtype=torch.float64, device=device)
     for j in range(lo, hi):
         a = contract_one(bits[j])
         mine[2 * j], mine[2 * j + 1] = a.real, a.imag
-    if world > 1:
-        dist.all_reduce(mine, op=dist.ReduceOp.SUM, group=group)   # disjoint supports: a gather
+    allreduce_sum_(mine, group)
     v = mine.cpu().numpy()
     return v[0::2] + 1j * v[1::2]

@@ -89,3 +89,18 @@ def test_two_ranks_gloo_slices_and_bitstrings():
     assert n_sl >= 1
     assert abs(amp - want) < 1e-12
     assert np.allclose(amps, wants, atol=1e-12)
+
+
+def test_slice_block_and_bitstring_steps():
+    """bench.py's partition: slice blocks are disjoint, contiguous and cover the list;
+    bitstring steps walk the rows in order, one contributing slice per step, no repeats."""
+    from paper_2208_01498_b200.dist import slice_block, bitstring_steps
+    live = [3, 5, 8, 13, 21, 34, 55]
+    for w in (1, 2, 3, 8):
+        blocks = [slice_block(live, w, r) for r in range(w)]
+        assert sum(blocks, []) == live
+    contrib = {0: [0, 2, 4], 1: [1], 2: [0, 1, 2, 3]}
+    items = bitstring_steps(lambda r, n: contrib[r][:n], [0, 1, 2], 6)
+    assert items == [(0, 0), (0, 2), (0, 4), (1, 1), (2, 0), (2, 1)]
+    assert len(set(items)) == len(items)
+    assert bitstring_steps(lambda r, n: contrib[r][:n], [1], 5) == [(1, 1)]

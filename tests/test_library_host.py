@@ -102,3 +102,22 @@ def test_degenerate_networks_and_orders_identical():
         co = tb.Order(cn, seed=0)
         os_, _ = find_order(on, seed=0)
         assert co.steps() == os_, c.name
+
+
+@pytest.mark.parametrize("ci", [1, 2, 3, 4])
+def test_bench_orders_bit_identical_to_oracle_files(ci):
+    """The benched orders: tn_find_order with bench.py's SPEC (seed, hierarchies, slicing
+    target) reproduces the order and the sliced indices the ORACLE found
+    (oracle/orders/config<ci>.json, scripts/write_oracle_orders.py), and reports the same
+    median fallbacks."""
+    import json
+    import bench
+    path = os.path.join(ROOT, "oracle", "orders", f"config{ci}.json")
+    o = json.load(open(path))
+    spec = bench.SPEC[ci]
+    assert (o["n_seeds"], o["max_log2_size"], o["diag_hyper"]) == (spec["n_seeds"], spec["slice_log"], spec["hyper"])
+    cn = tb.Network.from_circuit(config_circuit(ci), diag_hyper=spec["hyper"])
+    co = tb.Order(cn, seed=o["seed"], n_seeds=o["n_seeds"], max_log2_size=o["max_log2_size"])
+    assert co.steps() == [tuple(p) for p in o["steps"]]
+    assert co.slices() == o["slices"]
+    assert co.info()["median_fallbacks"] == o["median_fallbacks"]
