@@ -4,11 +4,12 @@ amplitudes/s on B200, % of tensor-pipe peak).
 
 Default workload (N=1): configs[1] -- 8x8 qubit lattice, depth 16, Haar U(2) + CZ
 brickwork, complex64 on block-scaled fp16x2 split-precision tensor cores, separator
-order (SM Algorithm 1, best of 256 randomized hierarchies) sliced to 2^34-entry tensors.
+order (SM Algorithm 1, best of 256 randomized hierarchies) sliced to 2^32-entry tensors.
 Its batch of 1024 seeded bitstrings is split into contiguous blocks per rank (weak
 scaling, no data-path collective; paper_2208_01498_b200/dist.py).  One STEP = one
-contributing slice of one amplitude (the whole separator tree over one sliced
-sub-network); a rank walks its bitstrings, each through its contributing slices.
+contributing slice of one amplitude (the separator tree over one sliced sub-network,
+minus its slice-invariant subtrees, which tn_prepare contracts once per bitstring and
+keeps); a rank walks its bitstrings, each through its contributing slices.
 Intermediates are GBs, far larger than the 126 MB L2, so no L2 flush is needed.
 
 --config 2 / 4 (Sycamore-53 m=14, (2+1)D 12x12 depth 20; complex64): one amplitude,
@@ -53,7 +54,7 @@ ORDER_SEED = 0
 # DESIGN.md R10: the slicing overhead differs by orders of magnitude between
 # hierarchies), the IQP hyperedge reading R3.  Must equal scripts/write_oracle_orders.py.
 SPEC = {
-    1: dict(dtype="c64", shard="bits", slice_log=34, hyper=False, n_seeds=256),
+    1: dict(dtype="c64", shard="bits", slice_log=32, hyper=False, n_seeds=256),
     2: dict(dtype="c64", shard="slices", slice_log=33, hyper=False, n_seeds=256),
     3: dict(dtype="c128", shard="bits", slice_log=0, hyper=True, n_seeds=4),
     4: dict(dtype="c64", shard="slices", slice_log=32, hyper=False, n_seeds=1024),
@@ -360,7 +361,6 @@ def run_ours(args):
             raise RuntimeError(f"rank {rank}: no slice to contract ({len(live)} contributing slices for {ws} ranks)")
         items = [(0, s) for s in mine]
         warm = [items[j % len(items)] for j in range(W)]
-        n_units_all = len(live)
     else:
         lo, hi = pdist.block_range(len(bits), ws, rank)
         rows = list(range(lo, hi))
@@ -371,7 +371,6 @@ def run_ours(args):
         if len(items) < K + W:
             raise RuntimeError(f"rank {rank}: {len(items)} work items for {K + W} steps")
         warm, items = items[K:], items[:K]
-        n_units_all = K * ws
     steps_mine = len(items)
     bits_dev = torch.from_numpy(np.ascontiguousarray(bits)).to(dev)
     # one complex128 accumulator per step (the same length K on every rank: the all-reduce of
@@ -379,8 +378,32 @@ def run_ours(args):
     amp = torch.zeros(max(K, 1), dtype=torch.complex128, device=dev)
     scratch = torch.zeros(1, dtype=torch.complex128, device=dev)
 
-    for row, s in warm:
-        plan.contract_device(bits_dev[row].data_ptr(), s, s + 1, scratch.data_ptr(), sptr)
+    flops_pro = float(pinfo["flops_prologue"])          # slice-invariant part, once per bitstring
+    flops_dep = flops_slice - flops_pro                   # the rest, once per slice
+
+    def run(work, amps, profiled, ev=None):
+        """contract `work` (row, slice) items: tn_prepare (the bitstring's slice-invariant
+        prologue) whenever the row changes, tn_contract_prepared per slice into amps[j];
+        returns (profiles, prologues run).  ev: lists of CUDA events around the calls."""
+        cur, n_pre, profs = None, 0, []
+        for j, (row, s) in enumerate(work):
+            if row != cur:
+                if ev is not None:
+                    ev["pro"].append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+                    ev["pro"][-1][0].record(stream)
+                profs.append(plan.prepare(bits_dev[row].data_ptr(), sptr, profiled=profiled))
+                if ev is not None:
+                    ev["pro"][-1][1].record(stream)
+                cur, n_pre = row, n_pre + 1
+            if ev is not None:
+                ev["slice"].append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+                ev["slice"][-1][0].record(stream)
+            profs.append(plan.contract_prepared(s, s + 1, amps[j:j + 1].data_ptr(), sptr, profiled=profiled))
+            if ev is not None:
+                ev["slice"][-1][1].record(stream)
+        return profs, n_pre
+
+    run(warm, scratch.expand(max(len(warm), 1)), False)
     torch.cuda.synchronize()
 
     def barrier():
@@ -388,54 +411,57 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- timed region: the steps through the profiled launcher (+ the slice all-reduce) ----
+    # ---- timed region: the steps through the profiled launchers (+ the slice all-reduce) ----
     launches0 = tb.kernel_launches()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = {"pro": [], "slice": []}
     with Clocks(local) as clk:
         e0.record(stream)
-        prof = None
-        for j, (row, s) in enumerate(items):
-            p = plan.contract_profiled(bits_dev[row].data_ptr(), s, s + 1, amp[j:j + 1].data_ptr(), sptr)
-            if prof is None:
-                prof = p
-            else:
-                for k, v in p.items():
-                    if k == "kernels":
-                        for name, d in v.items():
-                            for f, x in d.items():
-                                prof["kernels"][name][f] += x
-                    else:
-                        prof[k] += v
+        profs, n_pre = run(items, amp, True, ev)
         if by_slices:
             amp_mine = amp.clone()                  # (this rank's values, for the check below)
             pdist.allreduce_sum_(amp)               # partial amplitudes of all ranks' slices
         e1.record(stream)
         barrier()
     launches = tb.kernel_launches() - launches0
+    prof = profs[0]
+    for p in profs[1:]:
+        for k, v in p.items():
+            if k == "kernels":
+                for name, d in v.items():
+                    for f, x in d.items():
+                        prof["kernels"][name][f] += x
+            else:
+                prof[k] += v
     ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
-    total_flops = flops_slice * n_units_all
+    flops_mine = n_pre * flops_pro + steps_mine * flops_dep        # executed flops of this rank
+    t_fl = torch.tensor([flops_mine], dtype=torch.float64, device=dev)
+    pdist.allreduce_sum_(t_fl)
+    total_flops = float(t_fl.item())
     value = total_flops / (ms / 1e3)
+    t_pro = float(np.mean([a.elapsed_time(b) for a, b in ev["pro"]])) / 1e3
+    t_slice = float(np.mean([a.elapsed_time(b) for a, b in ev["slice"]])) / 1e3
 
     # ---- the timed amplitudes against the CUDA-graph path (same bitstring and slice) ----
     n_chk = min(steps_mine, 2)
     chk = torch.zeros(max(n_chk, 1), dtype=torch.complex128, device=dev)
-    for j in range(n_chk):
-        row, s = items[j]
-        plan.contract_device(bits_dev[row].data_ptr(), s, s + 1, chk[j:j + 1].data_ptr(), sptr)
+    run(items[:n_chk], chk, False)
     torch.cuda.synchronize()
     a_t, a_g = (amp_mine if by_slices else amp)[:n_chk].cpu().numpy(), chk[:n_chk].cpu().numpy()
     rel = float(np.max(np.abs(a_t - a_g) / np.maximum(np.abs(a_g), 1e-300))) if n_chk else 0.0
     if not rel <= 1e-9:
         raise RuntimeError(f"timed (profiled) amplitudes differ from the graph path: {a_t} vs {a_g}")
 
-    # amplitudes/s: an amplitude needs its contributing slices (provably zero ones are
-    # skipped by tn_contract / tn_amplitudes); mean over the whole batch
+    # amplitudes/s: an amplitude = its prologue + its contributing slices (provably zero
+    # ones are skipped by tn_contract / tn_amplitudes; mean count over the whole batch),
+    # timed on the device in the timed region (max over ranks)
     if n_slices > 1:
         contrib_mean = float(np.mean([plan.contributing_slices(b) for b in bits]))
     else:
         contrib_mean = 1.0
-    amps_per_s = value / (flops_slice * contrib_mean)
+    t_amp = pdist.max_over_ranks(t_pro + contrib_mean * t_slice, dev)
+    amps_per_s = ws / t_amp
 
     # ---- e2e: the public host-buffer call, H2D bits (pinned host memory) + D2H amplitude
     # inside the region ----
@@ -447,7 +473,7 @@ def run_ours(args):
         plan.contract(pinned[row], s, s + 1)
     barrier()
     e2e_s = pdist.max_over_ranks(time.perf_counter() - t0, dev)
-    e2e_value = flops_slice * len(e2e_items) * ws / e2e_s
+    e2e_value = flops_slice * len(e2e_items) * ws / e2e_s       # each call: prologue + one slice
 
     # ---- unsliced bitstring configs: throughput of tn_amplitudes with concurrent lanes ----
     lanes_line = None
@@ -526,6 +552,13 @@ def run_ours(args):
                        "complex128 on the FP64 tensor pipe (DMMA) and fp64 CUDA cores"),
         "amplitudes_per_s": amps_per_s,
         "contributing_slices_mean": contrib_mean,
+        "executed_flops_per_step": flops_mine / max(steps_mine, 1),
+        "slice_reuse": {"prologue_flops_fraction_of_slice": flops_pro / flops_slice,
+                        "frontier_gb": pinfo["frontier_bytes"] / 1e9, "prologues_timed": n_pre,
+                        "t_prologue_s": t_pro, "t_slice_s": t_slice,
+                        "note": "the slice-invariant subtrees are contracted once per bitstring (tn_prepare) and "
+                                "kept while its slices run (tn_contract_prepared); value = executed flops / time; "
+                                "amplitudes_per_s = N / (t_prologue + contributing_slices_mean x t_slice)"},
         "amplitudes_per_s_lanes": lanes_line,
         "slicing": {"slice_bits": slice_bits, "log2_sliced_work": oinfo["log2_slice_2M"] - 1.0 + slice_bits,
                     "log2_unsliced_work": oinfo["log2_total_2M"] - 1.0,

@@ -152,6 +152,14 @@ typedef struct {
   int32_t n_steps_small, n_steps_tc, n_launches_per_slice;
   double tc_flops_per_slice;     /* part of flops_per_slice on the tensor-core path */
   int32_t slice_bits;            /* log2 of the number of slice assignments */
+  /* Slice reuse: the steps whose subtree holds no sliced index
+   * are the same in every slice of a bitstring; they form a prologue run once per
+   * bitstring (flops_prologue, part of flops_per_slice), their outputs that feed
+   * per-slice steps (frontier_bytes) stay in the arena, and each slice runs the rest.
+   * 0 / 0 / 0 without slicing or with TN_SLICE_REUSE=0. */
+  double flops_prologue;
+  int64_t frontier_bytes;
+  int32_t n_launches_prologue;
 } tn_plan_info;
 int tn_plan_get_info(tn_plan plan, tn_plan_info* info);
 
@@ -195,6 +203,20 @@ typedef struct {
 } tn_profile;
 int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end,
                          void* amp_dev, void* stream, tn_profile* prof);
+/* Slice reuse across calls (PAPER.md l.178 index slicing):
+ * tn_contract / tn_contract_device / tn_contract_profiled / tn_amplitudes run the
+ * bitstring's slice-invariant prologue once per call, then the slices.  To spread the
+ * slices of one bitstring over several calls without repeating the prologue:
+ * tn_prepare copies the device bitstring bits_dev (uint8[n_qubits]) into the plan and
+ * runs its prologue; tn_contract_prepared then ADDS the slices [slice_begin, slice_end)
+ * of that bitstring to amp_dev (device complex128).  prof == NULL: CUDA-graph replay;
+ * otherwise eager launches with CUDA events, prof (host) receives the pass's profile as
+ * in tn_contract_profiled.  Any other contraction call on the plan (or on lane 0 through
+ * tn_amplitudes) in between invalidates the prepared state; the caller orders the calls
+ * on one stream. */
+int tn_prepare(tn_plan plan, const uint8_t* bits_dev, void* stream, tn_profile* prof);
+int tn_contract_prepared(tn_plan plan, int64_t slice_begin, int64_t slice_end, void* amp_dev, void* stream,
+                         tn_profile* prof);
 /* tn_amplitudes: full amplitudes (all slices) of n_bits bitstrings
  * (host uint8[n_bits * n_qubits]) into host double[2 * n_bits]; host<->device
  * copies included.  With lanes (tn_plan_set_lanes) bitstring j runs on lane j mod L,

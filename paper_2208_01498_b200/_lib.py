@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "tn_last_error", "tn_version", "tn_build_network", "tn_network_free", "tn_network_get_info",
     "tn_network_dims", "tn_network_tensor", "tn_order_params_default", "tn_find_order", "tn_order_free",
     "tn_order_get_info", "tn_order_steps", "tn_order_slices", "tn_plan_create", "tn_plan_free",
-    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_amplitudes", "tn_contract_pair",
+    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_prepare", "tn_contract_prepared", "tn_amplitudes", "tn_contract_pair",
     "tn_kernel_launches",
 ]
 
@@ -60,7 +60,8 @@ KERNEL_CLASSES = ["small_contract_kernel", "pack_f16x2s_kernel", "cgemm_f16x2s_k
 class _PlanInfo(C.Structure):
     _fields_ = [("flops_per_slice", C.c_double), ("n_slices", C.c_int64), ("arena_bytes", C.c_int64),
                 ("n_steps_small", C.c_int32), ("n_steps_tc", C.c_int32), ("n_launches_per_slice", C.c_int32),
-                ("tc_flops_per_slice", C.c_double), ("slice_bits", C.c_int32)]
+                ("tc_flops_per_slice", C.c_double), ("slice_bits", C.c_int32), ("flops_prologue", C.c_double),
+                ("frontier_bytes", C.c_int64), ("n_launches_prologue", C.c_int32)]
 
 
 def _load():
@@ -92,6 +93,8 @@ def _load():
         "tn_contract": (C.c_int, [P, P, I64, I64, P, P]),
         "tn_contract_device": (C.c_int, [P, P, I64, I64, P, P]),
         "tn_contract_profiled": (C.c_int, [P, P, I64, I64, P, P, C.POINTER(Profile)]),
+        "tn_prepare": (C.c_int, [P, P, P, C.POINTER(Profile)]),
+        "tn_contract_prepared": (C.c_int, [P, I64, I64, P, P, C.POINTER(Profile)]),
         "tn_amplitudes": (C.c_int, [P, P, I32, P, P]),
         "tn_contract_pair": (C.c_int, [I32, P, I32, P, P, I32, P, P, I32, P, P, I32, I32, P]),
         "tn_kernel_launches": (C.c_int64, []),
@@ -269,11 +272,28 @@ class Plan:
         pr = Profile()
         _check(lib.tn_contract_profiled(self.h, C.c_void_p(bits_dev_ptr), int(slice_begin), int(slice_end),
                                         C.c_void_p(amp_dev_ptr), C.c_void_p(stream), C.byref(pr)))
+        return self._profile_dict(pr)
+
+    @staticmethod
+    def _profile_dict(pr):
         out = {k: getattr(pr, k) for k, _ in pr._fields_ if not k.startswith("k_")}
         out["kernels"] = {name: {"ms": pr.k_ms[i], "flops": pr.k_flops[i], "bytes": pr.k_bytes[i],
                                  "intervals": int(pr.k_intervals[i])}
                           for i, name in enumerate(KERNEL_CLASSES)}
         return out
+
+    def prepare(self, bits_dev_ptr, stream=0, profiled=False):
+        """tn_prepare: the bitstring's slice-invariant prologue (profile dict if profiled)."""
+        pr = Profile() if profiled else None
+        _check(lib.tn_prepare(self.h, C.c_void_p(bits_dev_ptr), C.c_void_p(stream), C.byref(pr) if profiled else None))
+        return self._profile_dict(pr) if profiled else None
+
+    def contract_prepared(self, slice_begin, slice_end, amp_dev_ptr, stream=0, profiled=False):
+        """tn_contract_prepared: slices of the prepared bitstring (profile dict if profiled)."""
+        pr = Profile() if profiled else None
+        _check(lib.tn_contract_prepared(self.h, int(slice_begin), int(slice_end), C.c_void_p(amp_dev_ptr),
+                                        C.c_void_p(stream), C.byref(pr) if profiled else None))
+        return self._profile_dict(pr) if profiled else None
 
     def amplitudes(self, bits, stream=None):
         b = np.ascontiguousarray(bits, dtype=np.uint8)

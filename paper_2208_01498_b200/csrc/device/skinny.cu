@@ -217,6 +217,228 @@ __global__ void __launch_bounds__(SK_THREADS) skinny_kernel(const R* __restrict_
   }
 }
 
+// --------------------------------------------------------------- skinny v2 ----
+// The same contraction with the operand rows staged through shared memory by TMA: a
+// persistent CTA walks work items (batch, K range[, half of X's rows]); one producer lane
+// loads every stage -- the item's X rows (re and im planes) and Y rows x KS elements of K
+// -- as two 3-D tensor boxes {KS, rows, 2 planes} into a ring of STAGES buffers (mbarrier
+// full / empty), so each byte of X and Y is read from HBM once and enough bytes are in
+// flight to cover the latency (v1 read every X row from 2 warps and every Y row from 4,
+// straight from global, at 12% warp occupancy: 0.44-0.59 of HBM; per-row bulk copies of
+// 512 bytes were issue-bound at ~1 copy per 80 cycles per SM).  Sixteen consumer warps
+// (8 warps with 4 x 4 groups were issue / latency bound at 0.6 of HBM): each output group
+// (GM x GN <= 4 x 2, at most 16 groups per item) has WPG = 16 / groups warps, which take
+// its stages in turn; lanes take 16-byte vectors of consecutive k (conflict-free
+// LDS.128).  Complex64 products accumulate in fp32 over a stage (KS / 32 terms per lane,
+// <= 8) and fold into fp64 (the fp32-path bound with K = 8 holds: DESIGN.md
+// "Tolerances"); complex128 in fp64.  Per item the warp sums go to partial[b][s][wsub][o] (then the in-order
+// skinny_reduce_kernel: deterministic) or, with one item per batch and one warp per group,
+// straight to C.
+constexpr int SK2_WARPS = 16, SK2_THREADS = 32 * SK2_WARPS;
+
+// producer cursor over this CTA's stages (items blockIdx.x, + gridDim.x, ...; stages of KS)
+struct Sk2Cursor {
+  int64_t it, k, k1;
+  int b, h;
+};
+__device__ __forceinline__ bool sk2_item(Sk2Cursor& c, int64_t n_items, int m_split, int S, int64_t kc, int64_t K) {
+  if (c.it >= n_items) return false;
+  c.h = (int)(c.it % m_split);
+  const int64_t bs = c.it / m_split;
+  c.b = (int)(bs / S);
+  c.k = (bs % S) * kc;
+  c.k1 = min(K, c.k + kc);
+  return true;
+}
+
+template <typename R, int GM, int GN>
+__global__ void __launch_bounds__(SK2_THREADS, 1) skinny2_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                                const __grid_constant__ CUtensorMap tmY,
+                                                                double2* __restrict__ partial, int32_t m_bits,
+                                                                int32_t n_bits, int64_t K, int64_t kc, int32_t S,
+                                                                int32_t nb, int32_t m_split, int32_t ks,
+                                                                int32_t stages, void* const* __restrict__ ptrs,
+                                                                int32_t c_node, int32_t accumulate) {
+  using C2 = typename cplx_t<R>::type;
+  constexpr int VEC = 16 / sizeof(R);
+  extern __shared__ __align__(128) uint8_t sk_smem[];
+  const int M = 1 << m_bits, N = 1 << n_bits;
+  const int Mh = M / m_split;
+  const int rows = 2 * (Mh + N);
+  const int64_t stage_elems = (int64_t)rows * ks;
+  R* st_base = reinterpret_cast<R*>(sk_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sk_smem + (size_t)stages * stage_elems * sizeof(R));
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ngn = N / GN, n_groups = (Mh / GM) * ngn;
+  const int wpg = SK2_WARPS / n_groups;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], n_groups); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+  }
+  __syncthreads();
+  const int64_t n_items = (int64_t)nb * S * m_split;
+  // The producer is lane 0 of warp 0: before consuming stage g it tops the ring up to stage
+  // g + stages - 1 (whose slot frees when every group's warp has finished stage g - 1).
+  const bool producer = threadIdx.x == 0;
+  const uint32_t stage_bytes = (uint32_t)(stage_elems * sizeof(R));
+  Sk2Cursor pc{(int64_t)blockIdx.x, 0, 0, 0, 0};
+  bool p_more = producer && sk2_item(pc, n_items, m_split, S, kc, K);
+  int64_t g_p = 0;                               // next stage the producer loads
+  int p_slot = 0;
+  uint32_t p_phase = 0;
+  auto top_up = [&](int64_t g_limit) {
+    while (p_more && g_p < g_limit) {
+      tc::mbar_wait(&empty[p_slot], p_phase ^ 1);
+      tc::mbar_expect_tx(&full[p_slot], stage_bytes);
+      R* d = st_base + p_slot * stage_elems;
+      tc::tma_load_3d(&tmX, d, &full[p_slot], (int)pc.k, pc.h * Mh, 2 * pc.b);                    // [2][Mh][ks]
+      tc::tma_load_3d(&tmY, d + (int64_t)2 * Mh * ks, &full[p_slot], (int)pc.k, 0, 2 * pc.b);      // [2][N][ks]
+      ++g_p;
+      if (++p_slot == stages) { p_slot = 0; p_phase ^= 1; }
+      pc.k += ks;
+      if (pc.k >= pc.k1) {
+        pc.it += gridDim.x;
+        p_more = sk2_item(pc, n_items, m_split, S, kc, K);
+      }
+    }
+  };
+  // consumers: warp -> (group grp, sub-warp wsub of the WPG warps taking its stages in turn)
+  const int grp = warp % n_groups, wsub = warp / n_groups;
+  const int gm0 = (grp / ngn) * GM, gn0 = (grp % ngn) * GN;
+  const int iters = ks / (32 * VEC);
+  int64_t g = 0;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int h = (int)(it % m_split);
+    const int64_t bs = it / m_split;
+    const int b = (int)(bs / S), s = (int)(bs % S);
+    const int64_t k0 = (int64_t)s * kc, k1 = min(K, k0 + kc);
+    double ar[GM][GN], ai[GM][GN];
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) { ar[i][j] = 0.0; ai[i][j] = 0.0; }
+    int turn = 0;                                  // stage of this item modulo WPG
+    float br[GM][GN], bi[GM][GN];                  // complex64: fp32 sums since the last fold
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) { br[i][j] = 0.f; bi[i][j] = 0.f; }
+    int unfolded = 0;                              // stages summed into br / bi
+    for (int64_t k = k0; k < k1; k += ks, ++g) {
+      if (producer) top_up(g + stages);
+      const int cur = slot;
+      const uint32_t cph = phase;
+      if (++slot == stages) { slot = 0; phase ^= 1; }
+      const bool mine = turn == wsub;
+      if (++turn == wpg) turn = 0;
+      if (!mine) continue;
+      tc::mbar_wait(&full[cur], cph);
+      const R* st = st_base + cur * stage_elems;
+      for (int itr = 0; itr < iters; ++itr) {
+        const int kk = (itr * 32 + lane) * VEC;
+        if constexpr (sizeof(R) == 4) {
+          // all the iteration's loads first (16 warps x 128 registers hold them), then the FMAs
+          float4 yr[GN], yi[GN], xr4[GM], xi4[GM];
+#pragma unroll
+          for (int j = 0; j < GN; ++j) {
+            yr[j] = *reinterpret_cast<const float4*>(st + (int64_t)(2 * Mh + gn0 + j) * ks + kk);
+            yi[j] = *reinterpret_cast<const float4*>(st + (int64_t)(2 * Mh + N + gn0 + j) * ks + kk);
+          }
+#pragma unroll
+          for (int i = 0; i < GM; ++i) {
+            xr4[i] = *reinterpret_cast<const float4*>(st + (int64_t)(gm0 + i) * ks + kk);
+            xi4[i] = *reinterpret_cast<const float4*>(st + (int64_t)(Mh + gm0 + i) * ks + kk);
+          }
+#pragma unroll
+          for (int i = 0; i < GM; ++i) {
+            const float4 xr = xr4[i], xi = xi4[i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int j = 0; j < GN; ++j) {
+                const float a_r = (&xr.x)[u], a_i = (&xi.x)[u], b_r = (&yr[j].x)[u], b_i = (&yi[j].x)[u];
+                br[i][j] = fmaf(a_r, b_r, br[i][j]);
+                br[i][j] = fmaf(-a_i, b_i, br[i][j]);
+                bi[i][j] = fmaf(a_r, b_i, bi[i][j]);
+                bi[i][j] = fmaf(a_i, b_r, bi[i][j]);
+              }
+          }
+        } else {
+          double2 yr[GN], yi[GN];
+#pragma unroll
+          for (int j = 0; j < GN; ++j) {
+            yr[j] = *reinterpret_cast<const double2*>(st + (int64_t)(2 * Mh + gn0 + j) * ks + kk);
+            yi[j] = *reinterpret_cast<const double2*>(st + (int64_t)(2 * Mh + N + gn0 + j) * ks + kk);
+          }
+#pragma unroll
+          for (int i = 0; i < GM; ++i) {
+            const double2 xr = *reinterpret_cast<const double2*>(st + (int64_t)(gm0 + i) * ks + kk);
+            const double2 xi = *reinterpret_cast<const double2*>(st + (int64_t)(Mh + gm0 + i) * ks + kk);
+#pragma unroll
+            for (int j = 0; j < GN; ++j)
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const double a_r = (&xr.x)[u], a_i = (&xi.x)[u], b_r = (&yr[j].x)[u], b_i = (&yi[j].x)[u];
+                ar[i][j] = fma(a_r, b_r, ar[i][j]);
+                ar[i][j] = fma(-a_i, b_i, ar[i][j]);
+                ai[i][j] = fma(a_r, b_i, ai[i][j]);
+                ai[i][j] = fma(a_i, b_r, ai[i][j]);
+              }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[cur]);
+      if constexpr (sizeof(R) == 4) {
+        // fold the stage's fp32 sums (iters x 4 terms per lane: 8 for KS = 256) into fp64
+        // (folding every 2 stages measured no faster)
+        if (++unfolded == 1) {
+          unfolded = 0;
+#pragma unroll
+          for (int i = 0; i < GM; ++i)
+#pragma unroll
+            for (int j = 0; j < GN; ++j) {
+              ar[i][j] += (double)br[i][j]; ai[i][j] += (double)bi[i][j];
+              br[i][j] = 0.f; bi[i][j] = 0.f;
+            }
+        }
+      }
+    }
+    if constexpr (sizeof(R) == 4) {
+#pragma unroll
+      for (int i = 0; i < GM; ++i)
+#pragma unroll
+        for (int j = 0; j < GN; ++j) { ar[i][j] += (double)br[i][j]; ai[i][j] += (double)bi[i][j]; }
+    }
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+#pragma unroll
+      for (int j = 0; j < GN; ++j) {
+        double re = ar[i][j], im = ai[i][j];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, off);
+          im += __shfl_xor_sync(0xffffffffu, im, off);
+        }
+        if (lane == 0) {
+          const int o = (h * Mh + gm0 + i) * N + gn0 + j;
+          if (S * wpg == 1) {          // one partial per output: write C directly
+            C2* C = reinterpret_cast<C2*>(ptrs[c_node]) + (int64_t)b * M * N + o;
+            if (accumulate) { re += C->x; im += C->y; }
+            *C = C2{(R)re, (R)im};
+          } else {
+            partial[(((int64_t)b * S + s) * wpg + wsub) * (M * N) + o] = make_double2(re, im);
+          }
+        }
+      }
+  }
+}
+
 // C[b][o] (+)= sum_s partial[b][s][o]: one warp per output, lane l sums s = l, l + 32, ...
 // in order, then a fixed shuffle tree -- deterministic, and parallel when a long
 // contraction has few outputs (a scalar: S x 8 partials)

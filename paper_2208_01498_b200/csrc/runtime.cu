@@ -179,6 +179,21 @@ CUtensorMap make_plane_map(void* base, int k_bits, int r_bits, int nb_bits, int 
   return m;
 }
 
+// planar operand [b][2][rows][K] (fp32 or fp64) of the staged skinny kernel: 3-D map
+// (K, rows, 2 << nb_bits), boxes {box_k, box_rows, 2 planes}, no swizzle
+CUtensorMap make_planar_map(void* base, int k_bits, int r_bits, int nb_bits, int box_k, int box_rows, int esz_real) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cuuint64_t(1) << k_bits, cuuint64_t(1) << r_bits, cuuint64_t(2) << nb_bits};
+  cuuint64_t strides[2] = {(cuuint64_t(1) << k_bits) * esz_real, (cuuint64_t(1) << (k_bits + r_bits)) * esz_real};
+  cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_rows, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, esz_real == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base,
+                           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(TN_ECUDA, "cuTensorMapEncodeTiled (planar) failed: " + std::to_string((int)r));
+  return m;
+}
+
 // C of a tensor-core step, [rows][N] complex64 as [rows][2N] fp32, for TMA stores of 32 x
 // 16-complex boxes (SWIZZLE_128B)
 CUtensorMap make_c_map(void* base, int n_bits, int64_t rows) {
@@ -318,8 +333,68 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
   CK(cudaGetLastError());
 }
 
-// partial sums per (batch, K split) of a skinny step: one per warp sharing an output group
+// Launch shape of the staged skinny kernel (skinny2_kernel), a function of the step's bits:
+// 4 x 2 output groups (at most 16 per item; 32 groups -> two items per (batch, K range),
+// one per half of X's rows), WPG = 16 / groups warps per group taking its stages in turn,
+// stages of KS <= 256 elements of K (the TMA box limit; <= 48 KB), 2-8 stages in <= 200 KB,
+// and K split into S ranges per batch so that >= 2 waves of items cover the 148 SMs.
+struct Sk2Shape {
+  bool use = false;
+  int gm_bits = 0, gn_bits = 0, m_split = 1, wpg = 1, ks = 0, stages = 0, S = 1;
+  int64_t kc = 0;
+  size_t smem = 0;
+};
+Sk2Shape skinny2_shape(const TcStep& t) {
+  Sk2Shape h;
+  static const bool on = [] {
+    const char* e = std::getenv("TN_SKINNY_V2");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return h;
+  const int esz = t.esz / 2;                     // bytes per real element of a plane
+  h.gm_bits = std::min(t.m_bits, 2);
+  h.gn_bits = std::min(t.n_bits, 1);
+  int ng_bits = (t.m_bits - h.gm_bits) + (t.n_bits - h.gn_bits);
+  if (ng_bits > 4) {
+    if (ng_bits > 5 || t.m_bits - h.gm_bits < 1) return h;
+    h.m_split = 2;
+    ng_bits = 4;
+  }
+  h.wpg = 16 >> ng_bits;
+  const int64_t K = int64_t(1) << t.k_lo;
+  const int64_t ks_min = int64_t(32) * (16 / esz);       // one 16-byte vector per lane
+  if (K < ks_min) return h;
+  const int rows = 2 * ((1 << t.m_bits) / h.m_split + (1 << t.n_bits));
+  int64_t ks = ks_min;
+  while (ks * 2 <= std::min<int64_t>(K, 256) && rows * ks * 2 * esz <= 48 * 1024) ks *= 2;
+  const size_t stage = (size_t)rows * ks * esz;
+  if (stage > 100 * 1024) return h;
+  h.ks = (int)ks;
+  h.stages = (int)std::min<size_t>(8, (200 * 1024) / stage);
+  h.smem = h.stages * stage + 2 * 8 * h.stages;
+  const int64_t per_batch = (int64_t)h.m_split << t.nb_bits;
+  const int64_t want = std::max<int64_t>(1, (2 * 148 + per_batch - 1) / per_batch);
+  h.S = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / ks));
+  h.kc = (K + h.S - 1) / h.S;
+  h.kc = (h.kc + ks - 1) / ks * ks;
+  h.S = (int)((K + h.kc - 1) / h.kc);
+  h.use = true;
+  return h;
+}
+
+// tensor maps of a staged skinny step's planar operands (in the arena at x_off / y_off)
+void set_skinny_maps(TcStep& t, char* base) {
+  if (t.kind != K_SKINNY) return;
+  const Sk2Shape h = skinny2_shape(t);
+  if (!h.use) return;
+  t.ta = make_planar_map(base + t.x_off, t.k_lo, t.m_bits, t.nb_bits, h.ks, (1 << t.m_bits) / h.m_split, t.esz / 2);
+  t.tb = make_planar_map(base + t.y_off, t.k_lo, t.n_bits, t.nb_bits, h.ks, 1 << t.n_bits, t.esz / 2);
+}
+
+// partial sums per batch of a skinny step: K ranges x warps sharing an output group
 int skinny_ws(const TcStep& t) {
+  const Sk2Shape h = skinny2_shape(t);
+  if (h.use) return h.wpg;
   int gm, gn, ng, ws;
   tnd::skinny_groups(t.m_bits, t.n_bits, gm, gn, ng, ws);
   return ws;
@@ -345,7 +420,29 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
     if (mk) mk->mark(st, 0, t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE,
                      dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
                                              t.k_bits) : "");
-    if (t.kind == K_SKINNY) {
+    const Sk2Shape h2 = t.kind == K_SKINNY ? skinny2_shape(t) : Sk2Shape{};
+    if (t.kind == K_SKINNY && h2.use) {
+      const int64_t K = int64_t(1) << t.k_lo;
+      double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
+      const int64_t items = ((int64_t)h2.m_split << t.nb_bits) * t.S;
+      const unsigned grid = (unsigned)std::min<int64_t>(items, 148);
+#define TN_SKINNY2(GMB, GNB)                                                                                          \
+  if (h2.gm_bits == GMB && h2.gn_bits == GNB) {                                                                       \
+    ensure_smem_attr((const void*)tnd::skinny2_kernel<R, 1 << GMB, 1 << GNB>, 210 * 1024); /* >= any h2.smem */  \
+    tnd::skinny2_kernel<R, 1 << GMB, 1 << GNB><<<grid, tnd::SK2_THREADS, h2.smem, st>>>(                             \
+        t.ta, t.tb, partial, t.m_bits, t.n_bits, K, h2.kc, t.S, 1 << t.nb_bits, h2.m_split, h2.ks, h2.stages, ptrs_d, \
+        t.c_node, s > 0);                                                                                             \
+  }
+      TN_SKINNY2(0, 0) TN_SKINNY2(0, 1) TN_SKINNY2(1, 0) TN_SKINNY2(1, 1) TN_SKINNY2(2, 0) TN_SKINNY2(2, 1)
+#undef TN_SKINNY2
+      g_launches++;
+      if (t.S * h2.wpg == 1) continue;   // the kernel wrote C
+      if (mk) mk->mark(st, 3, TN_K_REDUCE);
+      const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
+          partial, t.S * h2.wpg, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      g_launches++;
+    } else if (t.kind == K_SKINNY) {
       const int64_t K = int64_t(1) << t.k_lo;
       const int64_t kc = ((K + t.S - 1) / t.S + 127) / 128 * 128;   // 16-byte aligned K ranges
       double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
@@ -743,8 +840,9 @@ void finish_cuda_core(TcStep& t, int dtype, int kind) {
   t.k_lo = kind == K_SKINNY ? std::max(std::min(t.k_bits, 6), t.k_bits - std::max(0, over)) : t.k_bits;
   t.n_slabs = 1 << (t.k_bits - t.k_lo);
   if (kind == K_SKINNY) {
+    const Sk2Shape h = skinny2_shape(t);
     const int64_t K = int64_t(1) << t.k_lo, want = std::max<int64_t>(1, (148 * 4) >> std::min(t.nb_bits, 20));
-    t.S = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 4096));
+    t.S = h.use ? h.S : (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 4096));
   } else {
     t.S = 1;
   }
@@ -805,6 +903,15 @@ struct tn_plan_s {
   std::vector<Wave> waves;
   std::vector<TcStep> tcs;
   std::vector<std::pair<int, int>> launches;  // (0, wave) | (1, tc)
+  // Slice-invariant prologue: launches [0, n_pro) contract the
+  // subtrees that hold no sliced index -- the same in every slice of one bitstring -- and
+  // run once per bitstring; their outputs that feed per-slice steps (the frontier) stay
+  // in the arena while launches [n_pro, end) run once per slice.
+  int n_pro = 0;
+  double flops_pro = 0;             // Eq. (3) flops of the prologue (part of `flops`)
+  int64_t frontier_bytes = 0;
+  int64_t kernels_pro = 0;
+  cudaGraphExec_t graph_pro = nullptr;
   int64_t n_slices = 1;
   int slice_bits = 0;
   double flops = 0, tc_flops = 0;
@@ -854,18 +961,21 @@ struct tn_plan_s {
     double2* amp_d = nullptr;
     std::vector<TcStep> tcs;
     cudaStream_t stream = nullptr;
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph = nullptr, graph_pro = nullptr;
   };
   std::vector<Lane> extra;
 
-  void record(cudaStream_t st) { record_lane(st, arena, ptrs_d, bits_d, slice_d, amp_d, tcs); }
+  // record one pass of a phase: 0 = the slice-invariant prologue (launches [0, n_pro)),
+  // 1 = one slice (launches [n_pro, end) + the fp64 root accumulation)
   void record_lane(cudaStream_t st, char* arena_l, void** ptrs_l, uint8_t* bits_l, int64_t* slice_l, double2* amp_l,
-                   const std::vector<TcStep>& tcs_l) {
+                   const std::vector<TcStep>& tcs_l, int phase) {
     tnd::set_leaf_ptrs_kernel<<<(n_leaves + 127) / 128, 128, 0, st>>>(
         ptrs_l, leaf_base_d, var_begin_d, var_kind_d, var_stride_d, n_leaves, bits_l, slice_l, sl_log2_d, sl_shift_d,
         esz, leaves);
     int64_t k = 1;
-    for (auto& L : launches) {
+    const size_t l0 = phase == 0 ? 0 : (size_t)n_pro, l1 = phase == 0 ? (size_t)n_pro : launches.size();
+    for (size_t li = l0; li < l1; ++li) {
+      const auto& L = launches[li];
       if (L.first == 0) {
         if (dtype == TN_C64) launch_wave<float>(waves[L.second], ptrs_l, tab_d, st);
         else launch_wave<double>(waves[L.second], ptrs_l, tab_d, st);
@@ -877,20 +987,41 @@ struct tn_plan_s {
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
+    if (phase == 0) {
+      CK(cudaGetLastError());
+      kernels_pro = k;
+      return;
+    }
     if (dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(ptrs_l, root, root_exp, amp_l, slice_l);
     else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(ptrs_l, root, root_exp, amp_l, slice_l);
     CK(cudaGetLastError());
     kernels_per_slice = k + 1;
   }
+  // capture a phase as a CUDA graph on stream st
+  cudaGraphExec_t capture(cudaStream_t st, char* arena_l, void** ptrs_l, uint8_t* bits_l, int64_t* slice_l,
+                          double2* amp_l, const std::vector<TcStep>& tcs_l, int phase) {
+    cudaGraph_t g;
+    cudaGraphExec_t e;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = g_launches.load();
+    record_lane(st, arena_l, ptrs_l, bits_l, slice_l, amp_l, tcs_l, phase);
+    g_launches = before;  // captured launches are counted when replayed
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&e, g, 0));
+    CK(cudaGraphDestroy(g));
+    return e;
+  }
 
   ~tn_plan_s() {
     for (auto& l : extra) {
       if (l.graph) cudaGraphExecDestroy(l.graph);
+      if (l.graph_pro) cudaGraphExecDestroy(l.graph_pro);
       if (l.stream) cudaStreamDestroy(l.stream);
       for (void* p : {(void*)l.arena, (void*)l.ptrs_d, (void*)l.bits_d, (void*)l.slice_d, (void*)l.amp_d})
         if (p) cudaFree(p);
     }
     if (graph) cudaGraphExecDestroy(graph);
+    if (graph_pro) cudaGraphExecDestroy(graph_pro);
     if (cap) cudaStreamDestroy(cap);
     for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
     for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
@@ -927,7 +1058,7 @@ void check_device(int device) {
   CK(cudaSetDevice(device));
 }
 
-void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
+void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord, bool allow_reuse) {
   P.net = &net;
   P.esz = P.dtype == TN_C64 ? 8 : 16;
   const int n = (int)net.tensors.size();
@@ -1092,13 +1223,58 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
       e[0] = TN_PATH_SMALL; e[1] = d.nb_bits; e[2] = d.m_bits; e[3] = d.n_bits; e[4] = d.k_bits;
     }
   }
+  // ---- slice-invariant prologue ----
+  // A node is slice-invariant when no leaf below it holds a sliced index: it is the same
+  // in every slice of a bitstring.  Phase 0 = those steps (once per bitstring), phase 1 =
+  // the rest (once per slice).  TN_SLICE_REUSE=0 puts every step in phase 1.
+  static const bool reuse_on = [] {
+    const char* e = std::getenv("TN_SLICE_REUSE");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<char> inv(P.n_nodes, 0);
+  for (int t = 0; t < n; ++t) {
+    inv[t] = 1;
+    for (int i : net.tensors[t].inds) if (sliced.count(i)) inv[t] = 0;
+  }
+  std::vector<int> phase(ord.steps.size(), 1);
+  double inv_flops = 0;
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    inv[n + k] = inv[ord.steps[k].first] && inv[ord.steps[k].second];
+    if (inv[n + k])
+      inv_flops += kind[k] ? P.tcs[big_index[k]].flops
+                           : 8.0 * std::ldexp(1.0, small_desc[k].nb_bits + small_desc[k].m_bits +
+                                                       small_desc[k].n_bits + small_desc[k].k_bits);
+  }
+  // the frontier costs arena memory: reuse only when it saves >= 2% of a slice's work
+  const bool reuse = reuse_on && allow_reuse && !sliced.empty() && inv_flops >= 0.02 * P.flops;
+  for (size_t k = 0; k < ord.steps.size(); ++k)
+    if (reuse && inv[n + k]) phase[k] = 0;
+  // big steps in launch order: phase 0 first, each phase in step order (topological)
+  {
+    std::vector<int> order_k;
+    for (int ph = 0; ph < 2; ++ph)
+      for (size_t k = 0; k < ord.steps.size(); ++k)
+        if (kind[k] && phase[k] == ph) order_k.push_back((int)k);
+    std::vector<TcStep> tcs2;
+    for (int k : order_k) {
+      tcs2.push_back(P.tcs[big_index[k]]);
+      big_index[k] = (int)tcs2.size() - 1;
+    }
+    P.tcs = std::move(tcs2);
+  }
+  int n_big0 = 0;
+  for (size_t k = 0; k < ord.steps.size(); ++k) if (kind[k] && phase[k] == 0) ++n_big0;
   // ---- schedule: small steps in waves between tensor-core steps ----
+  // slot s of a small step: it runs after big step s - 1 (launch order); per phase, the
+  // small steps of one slot go in waves by dependency depth
   std::vector<int> slot(ord.steps.size(), 0), depth(ord.steps.size(), 0);
   int n_big = (int)P.tcs.size();
-  std::vector<std::map<int, std::vector<int>>> slot_waves(n_big + 1);
+  std::vector<std::map<int, std::vector<int>>> slot_waves[2];
+  slot_waves[0].resize(n_big + 1);
+  slot_waves[1].resize(n_big + 1);
   for (size_t k = 0; k < ord.steps.size(); ++k) {
     if (kind[k]) continue;
-    int s = 0;
+    int s = phase[k] == 1 ? n_big0 : 0;
     for (int ch : {ord.steps[k].first, ord.steps[k].second}) {
       if (ch < n) continue;
       int ck = ch - n;
@@ -1108,37 +1284,47 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     for (int ch : {ord.steps[k].first, ord.steps[k].second}) {
       if (ch < n) continue;
       int ck = ch - n;
-      if (!kind[ck] && slot[ck] == s) d = std::max(d, depth[ck] + 1);
+      if (!kind[ck] && slot[ck] == s && phase[ck] == phase[k]) d = std::max(d, depth[ck] + 1);
     }
     slot[k] = s;
     depth[k] = d;
-    slot_waves[s][d].push_back((int)k);
+    slot_waves[phase[k]][s][d].push_back((int)k);
   }
   std::vector<int> step_pos(ord.steps.size(), 0);
-  for (int s = 0; s <= n_big; ++s) {
-    for (auto& kv : slot_waves[s]) {
-      Wave w;
-      int64_t acc = 0;
-      for (int k : kv.second) {
+  for (int ph = 0; ph < 2; ++ph) {
+    if (ph == 1) P.n_pro = (int)P.launches.size();
+    const int s_lo = ph == 0 ? 0 : n_big0, s_hi = ph == 0 ? n_big0 : n_big;
+    for (int s = s_lo; s <= s_hi; ++s) {
+      for (auto& kv : slot_waves[ph][s]) {
+        Wave w;
+        int64_t acc = 0;
+        for (int k : kv.second) {
+          w.prefix.push_back(acc);
+          const auto& d = small_desc[k];
+          int64_t outs = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
+          acc += (outs + d.opc - 1) / d.opc;
+          w.steps.push_back(d);
+          w.flops += 8.0 * std::ldexp(1.0, d.nb_bits + d.m_bits + d.n_bits + d.k_bits);
+          w.bytes += P.esz * (std::ldexp(1.0, L[d.a].bits) + std::ldexp(1.0, L[d.b].bits) + std::ldexp(1.0, L[d.c].bits));
+          step_pos[k] = (int)P.launches.size();
+        }
         w.prefix.push_back(acc);
-        const auto& d = small_desc[k];
-        int64_t outs = int64_t(1) << (d.nb_bits + d.m_bits + d.n_bits);
-        acc += (outs + d.opc - 1) / d.opc;
-        w.steps.push_back(d);
-        w.flops += 8.0 * std::ldexp(1.0, d.nb_bits + d.m_bits + d.n_bits + d.k_bits);
-        w.bytes += P.esz * (std::ldexp(1.0, L[d.a].bits) + std::ldexp(1.0, L[d.b].bits) + std::ldexp(1.0, L[d.c].bits));
-        step_pos[k] = (int)P.launches.size();
+        w.n_cta = acc;
+        P.launches.push_back({0, (int)P.waves.size()});
+        P.waves.push_back(std::move(w));
       }
-      w.prefix.push_back(acc);
-      w.n_cta = acc;
-      P.launches.push_back({0, (int)P.waves.size()});
-      P.waves.push_back(std::move(w));
+      if (s < s_hi) {
+        for (size_t k = 0; k < ord.steps.size(); ++k)
+          if (kind[k] && big_index[k] == s) step_pos[k] = (int)P.launches.size();
+        P.launches.push_back({1, s});
+      }
     }
-    if (s < n_big) {
-      for (size_t k = 0; k < ord.steps.size(); ++k)
-        if (kind[k] && big_index[k] == s) step_pos[k] = (int)P.launches.size();
-      P.launches.push_back({1, s});
-    }
+  }
+  for (size_t k = 0; k < ord.steps.size(); ++k) {
+    if (phase[k] != 0) continue;
+    P.flops_pro += kind[k] ? P.tcs[big_index[k]].flops
+                           : 8.0 * std::ldexp(1.0, small_desc[k].nb_bits + small_desc[k].m_bits +
+                                                       small_desc[k].n_bits + small_desc[k].k_bits);
   }
 
   for (size_t k = 0; k < ord.steps.size(); ++k) P.step_table[6 * k + 5] = step_pos[k];
@@ -1164,6 +1350,11 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
         slabbed = pt.n_slabs > 1 || pt.n_mslabs > 1;
       }
       hi = 2 * step_pos[pk] + ((kind[pk] && !slabbed) ? 0 : 1);
+      // the frontier of the prologue stays while the slices run
+      if (phase[k] == 0 && phase[pk] == 1) {
+        hi = last;
+        P.frontier_bytes += (int64_t(1) << L[c].bits) * P.esz;
+      }
     }
     sizes.push_back((int64_t(1) << L[c].bits) * P.esz);
     ivs.push_back({born, hi});
@@ -1206,6 +1397,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     }
   }
   for (auto& t : P.tcs) {
+    set_skinny_maps(t, P.arena);
     if (t.kind != K_TC) continue;
     t.ta = make_plane_map(P.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
     t.tb = make_plane_map(P.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
@@ -1269,18 +1461,12 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord) {
     w.prefix_d = upload(w.prefix);
   }
   if (n == 1 && ord.steps.empty()) P.root = 0;
-  // ---- capture one slice as a CUDA graph ----
+  // ---- capture the prologue and one slice as CUDA graphs ----
   ensure_gemm_attr<128>();
   ensure_gemm_attr<64>();
   CK(cudaStreamCreateWithFlags(&P.cap, cudaStreamNonBlocking));
-  cudaGraph_t g;
-  CK(cudaStreamBeginCapture(P.cap, cudaStreamCaptureModeThreadLocal));
-  int64_t before = g_launches.load();
-  P.record(P.cap);
-  g_launches = before;  // captured launches are counted when replayed
-  CK(cudaStreamEndCapture(P.cap, &g));
-  CK(cudaGraphInstantiate(&P.graph, g, 0));
-  CK(cudaGraphDestroy(g));
+  if (P.n_pro > 0) P.graph_pro = P.capture(P.cap, P.arena, P.ptrs_d, P.bits_d, P.slice_d, P.amp_d, P.tcs, 0);
+  P.graph = P.capture(P.cap, P.arena, P.ptrs_d, P.bits_d, P.slice_d, P.amp_d, P.tcs, 1);
 }
 
 // one more lane of per-contraction state (see tn_plan_s::Lane)
@@ -1303,6 +1489,7 @@ void add_lane(tn_plan_s& P) {
   CK(cudaMemset(l.amp_d, 0, 16));
   l.tcs = P.tcs;
   for (auto& t : l.tcs) {
+    set_skinny_maps(t, l.arena);
     if (t.kind != K_TC) continue;
     t.ta = make_plane_map(l.arena + t.x_off, t.k_lo, t.m_lo, t.nb_bits, 128, 4);
     t.tb = make_plane_map(l.arena + t.y_off, t.k_lo, t.n_bits, t.nb_bits, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);
@@ -1310,20 +1497,15 @@ void add_lane(tn_plan_s& P) {
       t.tc = make_c_map(l.arena + P.node_off[t.c_node], t.n_bits, int64_t(1) << (t.nb_bits + t.m_bits));
   }
   CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
-  cudaGraph_t g;
-  CK(cudaStreamBeginCapture(l.stream, cudaStreamCaptureModeThreadLocal));
-  const int64_t before = g_launches.load();
-  P.record_lane(l.stream, l.arena, l.ptrs_d, l.bits_d, l.slice_d, l.amp_d, l.tcs);
-  g_launches = before;
-  CK(cudaStreamEndCapture(l.stream, &g));
-  CK(cudaGraphInstantiate(&l.graph, g, 0));
-  CK(cudaGraphDestroy(g));
+  if (P.n_pro > 0) l.graph_pro = P.capture(l.stream, l.arena, l.ptrs_d, l.bits_d, l.slice_d, l.amp_d, l.tcs, 0);
+  l.graph = P.capture(l.stream, l.arena, l.ptrs_d, l.bits_d, l.slice_d, l.amp_d, l.tcs, 1);
   P.extra.push_back(std::move(l));
 }
 
-void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_profile& pr) {
-  std::memset(&pr, 0, sizeof(pr));
-  for (int64_t s = s0; s < s1; ++s) {
+// one eager pass of a phase (0: prologue, 1: the slice at *slice_d) with CUDA events
+// around every kernel class; the device times and algorithmic flops / bytes are ADDED to pr
+void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
+  {
     Marks mk;
     mk.mark(st, 4, TN_K_OTHER);
     tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
@@ -1331,7 +1513,9 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
         P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
     g_launches++;
     pr.n_other++;
-    for (const auto& L : P.launches) {
+    const size_t l0 = phase == 0 ? 0 : (size_t)P.n_pro, l1 = phase == 0 ? (size_t)P.n_pro : P.launches.size();
+    for (size_t li = l0; li < l1; ++li) {
+      const auto& L = P.launches[li];
       if (L.first == 0) {
         {
           const auto& w = P.waves[L.second];
@@ -1380,11 +1564,13 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
         }
       }
     }
-    mk.mark(st, 4, TN_K_OTHER);
-    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
-    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
-    g_launches++;
-    pr.n_other++;
+    if (phase == 1) {
+      mk.mark(st, 4, TN_K_OTHER);
+      if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
+      else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
+      g_launches++;
+      pr.n_other++;
+    }
     mk.mark(st, -1, TN_K_OTHER);
     CK(cudaEventSynchronize(mk.v.back().first));
     for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
@@ -1406,6 +1592,13 @@ void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_pr
     }
     for (auto& e : mk.v) cudaEventDestroy(e.first);
   }
+}
+
+// eager, profiled: the prologue (if asked and the plan has one), then slices [s0, s1)
+void profile_slices(tn_plan_s& P, int64_t s0, int64_t s1, cudaStream_t st, tn_profile& pr, bool prologue) {
+  std::memset(&pr, 0, sizeof(pr));
+  if (prologue && P.n_pro > 0 && s1 > s0) profile_phase(P, 0, st, pr);
+  for (int64_t s = s0; s < s1; ++s) profile_phase(P, 1, st, pr);
 }
 
 // allowed values of every sliced index for a host bitstring (bit v of mask[j]); a slice
@@ -1436,14 +1629,28 @@ bool masks_full(const tn_plan_s& P, const std::vector<uint32_t>& m) {
 
 // graph replays of slices [s0, s1) on `st`; with a host bitstring, provably zero slices
 // are skipped (the slice counter is set before each replay)
+// the slice-invariant prologue of the bitstring in P.bits_d (graph)
+void run_prologue(tn_plan_s& P, cudaStream_t st) {
+  if (P.n_pro == 0) return;
+  CK(cudaGraphLaunch(P.graph_pro, st));
+  g_launches += P.kernels_pro;
+}
+
+// bits == nullptr: the bitstring already in P.bits_d and its prologue already run
+// (tn_contract_prepared); otherwise copy it in and run the prologue first
 void run_slices(tn_plan_s& P, const uint8_t* bits, bool bits_on_device, int64_t s0, int64_t s1, cudaStream_t st) {
   if (s0 < 0 || s1 > P.n_slices || s0 > s1) throw Err(TN_EINVAL, "slice range out of bounds");
   CK(cudaSetDevice(P.device));
-  if (P.net->n_qubits > 0)
+  if (bits && P.net->n_qubits > 0)
     CK(cudaMemcpyAsync(P.bits_d, bits, P.net->n_qubits, bits_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(P.amp_d, 0, 16, st));
   std::vector<uint32_t> m;
-  if (!bits_on_device && !P.forced.empty()) m = slice_masks(P, bits);
+  if (bits && !bits_on_device && !P.forced.empty()) m = slice_masks(P, bits);
+  if (bits && s1 > s0) {
+    bool any = m.empty();
+    for (int64_t s = s0; s < s1 && !any; ++s) any = slice_allowed(P, m, s);
+    if (any) run_prologue(P, st);
+  }
   if (m.empty() || masks_full(P, m)) {
     set_i64_kernel<<<1, 1, 0, st>>>(P.slice_d, s0);
     for (int64_t s = s0; s < s1; ++s) {
@@ -1600,7 +1807,16 @@ int tn_plan_create(tn_network h, tn_order o, int32_t dtype, int32_t device, tn_p
     auto p = std::make_unique<tn_plan_s>();
     p->dtype = dtype;
     p->device = device;
-    build_plan(*p, h->net, o->ord);
+    try {
+      build_plan(*p, h->net, o->ord, true);
+    } catch (const Err& e) {
+      // the slice-reuse frontier does not fit: plan without it
+      if (e.code != TN_ENOMEM) throw;
+      p = std::make_unique<tn_plan_s>();
+      p->dtype = dtype;
+      p->device = device;
+      build_plan(*p, h->net, o->ord, false);
+    }
     *out = p.release();
   });
 }
@@ -1617,6 +1833,9 @@ int tn_plan_get_info(tn_plan p, tn_plan_info* info) {
     info->n_launches_per_slice = (int32_t)p->kernels_per_slice;
     info->tc_flops_per_slice = p->tc_flops;
     info->slice_bits = p->slice_bits;
+    info->flops_prologue = p->flops_pro;
+    info->frontier_bytes = p->frontier_bytes;
+    info->n_launches_prologue = (int32_t)p->kernels_pro;
   });
 }
 
@@ -1662,7 +1881,43 @@ int tn_contract_profiled(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin
     if (p->net->n_qubits > 0) CK(cudaMemcpyAsync(p->bits_d, bits_dev, p->net->n_qubits, cudaMemcpyDeviceToDevice, st));
     set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
     CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
-    profile_slices(*p, slice_begin, slice_end, st, *prof);
+    profile_slices(*p, slice_begin, slice_end, st, *prof, true);
+    add_amp_kernel<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(amp_dev), p->amp_d);
+    g_launches++;
+    CK(cudaGetLastError());
+  });
+}
+
+int tn_prepare(tn_plan p, const uint8_t* bits_dev, void* stream, tn_profile* prof) {
+  return guard([&] {
+    if (!p || (!bits_dev && p->net->n_qubits > 0)) throw Err(TN_EINVAL, "null");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(p->device));
+    if (p->net->n_qubits > 0) CK(cudaMemcpyAsync(p->bits_d, bits_dev, p->net->n_qubits, cudaMemcpyDeviceToDevice, st));
+    if (prof) {
+      std::memset(prof, 0, sizeof(*prof));
+      if (p->n_pro > 0) profile_phase(*p, 0, st, *prof);
+    } else {
+      run_prologue(*p, st);
+    }
+    CK(cudaGetLastError());
+  });
+}
+
+int tn_contract_prepared(tn_plan p, int64_t slice_begin, int64_t slice_end, void* amp_dev, void* stream,
+                         tn_profile* prof) {
+  return guard([&] {
+    if (!p || !amp_dev) throw Err(TN_EINVAL, "null");
+    if (slice_begin < 0 || slice_end > p->n_slices || slice_begin > slice_end) throw Err(TN_EINVAL, "slice range");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(p->device));
+    if (prof) {
+      set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
+      CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
+      profile_slices(*p, slice_begin, slice_end, st, *prof, false);
+    } else {
+      run_slices(*p, nullptr, true, slice_begin, slice_end, st);
+    }
     add_amp_kernel<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(amp_dev), p->amp_d);
     g_launches++;
     CK(cudaGetLastError());
@@ -1705,11 +1960,16 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
       int64_t* sd = l ? p->extra[l - 1].slice_d : p->slice_d;
       double2* ad = l ? p->extra[l - 1].amp_d : p->amp_d;
       cudaGraphExec_t gr = l ? p->extra[l - 1].graph : p->graph;
+      cudaGraphExec_t gp = l ? p->extra[l - 1].graph_pro : p->graph_pro;
       if (nq > 0) CK(cudaMemcpyAsync(bd, bits_all + (size_t)j * nq, nq, cudaMemcpyDeviceToDevice, ss));
       CK(cudaMemsetAsync(ad, 0, 16, ss));
       std::vector<uint32_t> m;
       if (!p->forced.empty()) m = slice_masks(*p, bits + (size_t)j * nq);
       const bool full = m.empty() || masks_full(*p, m);
+      if (gp && p->n_slices > 0) {
+        CK(cudaGraphLaunch(gp, ss));
+        g_launches += p->kernels_pro;
+      }
       if (full) set_i64_kernel<<<1, 1, 0, ss>>>(sd, 0);
       for (int64_t s = 0; s < p->n_slices; ++s) {
         if (!full) {
@@ -1875,6 +2135,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       t.x_off = 0;
       t.y_off = (int64_t)((xb + ALIGN - 1) / ALIGN * ALIGN);
       t.p_off = t.y_off + (int64_t)((yb + ALIGN - 1) / ALIGN * ALIGN);
+      set_skinny_maps(t, scratch);
       if (t.kind == K_TC) {
         t.ta = make_plane_map(scratch + t.x_off, t.k_lo, t.m_lo, nb, 128, 4);
         t.tb = make_plane_map(scratch + t.y_off, t.k_lo, my, nb, t.pair ? tnd::tc::Cfg2::BNH : t.BN, 4);

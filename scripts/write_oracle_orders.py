@@ -22,7 +22,7 @@ from oracle.network import build_network           # noqa: E402
 from oracle import ssa                             # noqa: E402
 
 # (seed, n_seeds, slicing target, diag_hyper) -- must equal bench.py SPEC
-PARAMS = {1: (0, 256, 34, False), 2: (0, 256, 33, False), 3: (0, 4, 0, True), 4: (0, 1024, 32, False)}
+PARAMS = {1: (0, 256, 32, False), 2: (0, 256, 33, False), 3: (0, 4, 0, True), 4: (0, 1024, 32, False)}
 
 
 def main():

@@ -253,7 +253,10 @@ SKINNY_CASES = [
     (0, 0, 0, 14, 3),         # full contraction to a scalar (one output), permuted
     (2, 2, 3, 11, 4),         # batch 4, permuted layouts
     (0, 6, 2, 10, 5),         # M = 64 rows, N = 4
-    (1, 3, 3, 5, None),       # K = 32: a single partial K tile
+    (1, 3, 3, 5, None),       # K = 32: a single partial K tile (v1 kernel: below one v2 stage)
+    (0, 4, 3, 16, None),      # the configs[4] (4, 3, 26) K-slab shape at K = 65536 (8 groups of 4 x 4)
+    (0, 4, 4, 12, 9),         # M = N = 16: 16 groups -> items on halves of X's rows, permuted
+    (3, 1, 2, 10, 1),         # batch 8, one 2 x 4 group: 8 warps share its stage iterations
 ]
 WIDE_CASES = [
     (0, 7, 9, 3, None),       # 128 x 512 outputs, K = 8
@@ -269,8 +272,8 @@ def test_pair_skinny_path(case, dtype):
     nb, m, n, k, ps = SKINNY_CASES[case]
     ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
     got, ref, bound = _run_pair(ia, ib, ic, dims, dtype, tb.TN_PATH_SKINNY, seed=50 + case)
-    # complex128: fp64 accumulation; complex64: fp32 blocks of 8 terms per lane summed in
-    # fp64 -- the fp32-path bound for K = 8
+    # complex128: fp64 accumulation; complex64: fp32 blocks of <= 8 terms per lane summed
+    # in fp64 -- the fp32-path bound for K = 8
     tol = 1e-12 if dtype == tb.TN_C128 else c64_tol(8)
     assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
 
@@ -297,7 +300,7 @@ def test_pair_skinny_k_slabs():
         for dt in (tb.TN_C64, tb.TN_C128):
             ia, ib, ic, dims = T._gemm_case(1, 3, 2, 14, 8)
             got, ref, bound = T._run_pair(ia, ib, ic, dims, dt, tb.TN_PATH_SKINNY, seed=33)
-            tol = 1e-12 if dt == tb.TN_C128 else 6 * 2.0 ** -24
+            tol = 1e-12 if dt == tb.TN_C128 else T.c64_tol(8)
             assert np.all(np.abs(got - ref) <= tol * bound + 1e-30), (np.abs(got - ref) / bound).max()
         print('ok')
     """)
@@ -485,9 +488,9 @@ def test_config3_full_size_sampled_amplitudes():
 
 # ------------------------------------------------ full-size config 1 ------
 def test_config1_full_size_biggest_gemm_sampled():
-    """configs[1] (8x8 depth 16, complex64): the bench's plan (best of 256 hierarchies, the
-    largest slicing target that fits); take its largest tensor-core step whose operands
-    and result all fit in 2^31 entries (the bench plan's biggest steps hold 2^34-entry
+    """configs[1] (8x8 depth 16, complex64): the bench's plan (best of 256 hierarchies,
+    bench.SPEC's slicing target); take its largest tensor-core step whose operands
+    and result all fit in 2^31 entries (the bench plan's biggest steps hold 2^32-entry
     operands that cannot be materialised again beside it) and run that GEMM shape through
     tn_contract_pair -- the same kernels, tiles, slabs and grid as in the plan -- on random
     operands; 64 sampled outputs against complex128 dot products."""
@@ -495,13 +498,10 @@ def test_config1_full_size_biggest_gemm_sampled():
     c = config_circuit(1)
     cn = tb.Network.from_circuit(c)
     plan = None
-    for tgt in (34, 33, 32, 31):
-        co = tb.Order(cn, seed=0, n_seeds=256, max_log2_size=tgt)
-        try:
-            plan = tb.Plan(cn, co, dtype=tb.TN_C64)
-            break
-        except tb.TnError:
-            continue
+    import bench
+    tgt = bench.SPEC[1]["slice_log"]
+    co = tb.Order(cn, seed=0, n_seeds=256, max_log2_size=tgt)
+    plan = tb.Plan(cn, co, dtype=tb.TN_C64)
     st = plan.steps()
     tc = st[st[:, 0] == tb.TN_PATH_TC]
     fits = [r for r in tc if max(r[1] + r[2] + r[4], r[1] + r[3] + r[4], r[1] + r[2] + r[3]) <= 31]
@@ -633,8 +633,8 @@ def test_lanes_concurrent_amplitudes():
 
 
 def test_bench_plan_slice_self_consistent():
-    """The bench's own plan (configs[1], best of 256 hierarchies, largest slicing target
-    that fits, 2^30-entry pack cap: K-slabs, row slabs, CTA pairs, persistent tiles) is
+    """The bench's own plan (configs[1], best of 256 hierarchies, bench.SPEC's slicing
+    target, 2^30-entry pack cap: K-slabs, row slabs, CTA pairs, persistent tiles) is
     beyond the oracle; run one of its slices three ways -- default, pack cap 2^28 (other
     slab structure), single-CTA GEMM (no cta_group::2 / persistent kernels) -- and require
     agreement to 1e-5 of the RMS slice (child processes: plans of ~180 GB each)."""
@@ -645,15 +645,13 @@ def test_bench_plan_slice_self_consistent():
         from tn_inputs import config_circuit, random_bitstrings
         c = config_circuit(1)
         net = tb.Network.from_circuit(c)
-        for tgt in (34, 33, 32, 31):
-            o = tb.Order(net, seed=0, n_seeds=256, max_log2_size=tgt)
-            try:
-                p = tb.Plan(net, o, dtype=tb.TN_C64)
-                break
-            except tb.TnError:
-                continue
+        import bench
+        tgt = bench.SPEC[1]["slice_log"]
+        o = tb.Order(net, seed=0, n_seeds=256, max_log2_size=tgt)
+        p = tb.Plan(net, o, dtype=tb.TN_C64)
         x = random_bitstrings(c.n, 1, 1)[0]
-        a = p.contract(x, 0, 4)          # 4 slices, half of them provably zero (skipped)
+        ids = p.contributing_slice_ids(x, 0, 4)
+        a = p.contract(x, 0, ids[-1] + 1)   # the first 4 contributing slices (zero ones skipped)
         print(repr((tgt, p.info()["slice_bits"], a.real, a.imag)))
     """)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -8,10 +8,10 @@ plans").
   slicing target 2^31 through the complex64 plan and through the complex128 plan of the
   same order (the DMMA / fp64 path, oracle-verified at 1e-13 per step), agreeing to 1e-5
   of the RMS slice;
-* one full configs[1] amplitude through the bench plan itself (2^34 slicing target, best
-  of 256 hierarchies, 32 contributing slices) against the same amplitude through a
-  differently sliced plan (2^33 target: other hierarchy, other slices, other slab
-  structure).
+* one full configs[1] amplitude through the bench plan itself (2^32 slicing target, best
+  of 256 hierarchies, 64 contributing slices, slice-invariant prologue) against the same
+  amplitude through a differently sliced plan (2^34 target: other hierarchy, other
+  slices, other slab structure, with TN_SLICE_REUSE=0: no prologue).
 """
 import os
 import subprocess
@@ -90,6 +90,7 @@ def test_full_size_slice_complex64_vs_complex128(ci):
     complex64 tensor-core plan against the complex128 plan of the same order, each in its
     own process (plans of up to ~180 GB)."""
     _cuda()
+    torch.cuda.empty_cache()           # the child plans need the whole device
     res = {}
     for dt in (tb.TN_C64, tb.TN_C128):
         code = _C64_VS_C128.replace("CI", str(ci)).replace("TGT", "31").replace("NSEEDS", "64").replace("DT", str(dt))
@@ -120,22 +121,80 @@ _FULL_AMP = textwrap.dedent("""
     p = tb.Plan(net, o, dtype=tb.TN_C64)
     x = random_bitstrings(c.n, 1024, 1)[0]          # the bench batch's first bitstring
     a = p.amplitudes(np.array([x]))[0]              # all slices (zero ones skipped)
-    print(repr((p.info()["slice_bits"], p.contributing_slices(x), a.real, a.imag)))
+    print(repr((p.info()["slice_bits"], p.contributing_slices(x), p.info()["flops_prologue"] > 0, a.real, a.imag)))
 """)
 
 
 def test_config1_full_amplitude_two_slicings():
-    """A full configs[1] amplitude through the bench plan (2^34) and through a 2^33 plan."""
+    """A full configs[1] amplitude through the bench plan (2^32, slice reuse) and through a
+    2^34 plan without slice reuse (TN_SLICE_REUSE=0)."""
     _cuda()
+    torch.cuda.empty_cache()           # the child plans need the whole device
+    import bench
     res = []
-    for tgt in (34, 33):
+    for tgt, env in ((bench.SPEC[1]["slice_log"], {}), (34, {"TN_SLICE_REUSE": "0"})):
         r = subprocess.run([sys.executable, "-c", _FULL_AMP.replace("TGT", str(tgt))], capture_output=True, text=True,
-                           cwd=ROOT, timeout=1800)
+                           cwd=ROOT, timeout=1800, env=dict(os.environ, **env))
         assert r.returncode == 0, r.stdout + r.stderr
         res.append(eval(r.stdout.strip().splitlines()[-1]))
-    (b34, c34, *v34), (b33, c33, *v33) = res
-    assert b34 == 6 and c34 == 32 and b33 > b34
-    a34, a33 = complex(*v34), complex(*v33)
+    (b1, c1, pro1, *v1), (b2, c2, pro2, *v2) = res
+    assert b1 == 8 and c1 == 64 and pro1 and b2 == 6 and c2 == 32 and not pro2
+    a1, a2 = complex(*v1), complex(*v2)
     scale = 2.0 ** (-64 / 2)
-    assert abs(a34 - a33) <= 1e-5 * max(abs(a33), scale), (a34, a33)
-    print(f"configs[1] <x|C|0> = {a34} (2^34 plan), {a33} (2^33 plan)")
+    rel = abs(a1 - a2) / max(abs(a2), scale)
+    with open(os.path.join(ROOT, "gpurun_out", "config1_full_amplitude.txt"), "w") as f:
+        f.write(f"configs[1] <x|C|0> = {a1} (bench plan, 2^32 + reuse), {a2} (2^34, no reuse), rel diff {rel:.3e}\n")
+    assert rel <= 1e-5, (a1, a2)
+
+
+def test_slice_reuse_prologue():
+    """Slice reuse: the slice-invariant prologue runs once per
+    bitstring.  (a) plan.info reports a prologue and a frontier; (b) tn_prepare + the
+    slices through tn_contract_prepared (graph and profiled) sum to the tn_contract_device
+    amplitude and to the unsliced oracle; (c) a plan built with TN_SLICE_REUSE=0 (child
+    process) gives bit-identical amplitudes through tn_amplitudes."""
+    dev = _cuda()
+    from oracle.network import build_network
+    from oracle.contract import contract_tree
+    c = lattice_cz(6, 6, 12, 8)
+    net = tb.Network.from_circuit(c)
+    order = tb.Order(net, seed=0, max_log2_size=19)
+    plan = tb.Plan(net, order, dtype=tb.TN_C64)
+    info = plan.info()
+    assert info["n_slices"] >= 4 and info["flops_prologue"] > 0 and info["frontier_bytes"] > 0
+    assert info["flops_prologue"] < info["flops_per_slice"]
+    xs = random_bitstrings(c.n, 3, 6)
+    st = torch.cuda.current_stream().cuda_stream
+    on = build_network(c)
+    ns = info["n_slices"]
+    for x in xs:
+        bits = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        full = torch.zeros(1, dtype=torch.complex128, device=dev)
+        plan.contract_device(bits.data_ptr(), 0, ns, full.data_ptr(), st)
+        parts = torch.zeros(ns, dtype=torch.complex128, device=dev)
+        plan.prepare(bits.data_ptr(), st)
+        for s in range(ns):
+            plan.contract_prepared(s, s + 1, parts[s:s + 1].data_ptr(), st, profiled=(s % 2 == 1))
+        prof = torch.zeros(1, dtype=torch.complex128, device=dev)
+        p = plan.prepare(bits.data_ptr(), st, profiled=True)
+        assert abs(sum(d["flops"] for d in p["kernels"].values()) - info["flops_prologue"]) <= 1e-9 * info["flops_prologue"]
+        plan.contract_prepared(0, ns, prof.data_ptr(), st)
+        torch.cuda.synchronize()
+        a_full, a_parts, a_prof = full.item(), parts.sum().item(), prof.item()
+        assert abs(a_parts - a_full) <= 1e-12 * abs(a_full) and abs(a_prof - a_full) <= 1e-12 * abs(a_full)
+        want = contract_tree(on, order.steps(), x)
+        assert abs(a_full - want) <= 1e-5 * max(abs(want), 2.0 ** (-c.n / 2))
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        import numpy as np, paper_2208_01498_b200 as tb
+        from tn_inputs import lattice_cz, random_bitstrings
+        c = lattice_cz(6, 6, 12, 8)
+        net = tb.Network.from_circuit(c)
+        p = tb.Plan(net, tb.Order(net, seed=0, max_log2_size=19), dtype=tb.TN_C64)
+        assert p.info()["flops_prologue"] == 0
+        print(repr([complex(a) for a in p.amplitudes(random_bitstrings(c.n, 3, 6))]))
+    """)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600,
+                       env=dict(os.environ, TN_SLICE_REUSE="0"))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert eval(r.stdout.strip().splitlines()[-1]) == [complex(a) for a in plan.amplitudes(xs)]
