@@ -336,8 +336,12 @@ __global__ void __launch_bounds__(SK2_THREADS, 1) skinny2_kernel(const __grid_co
       if (++slot == stages) { slot = 0; phase ^= 1; }
       const bool mine = turn == wsub;
       if (++turn == wpg) turn = 0;
-      if (!mine) continue;
+      // every warp waits for every stage in order, owner or not: a warp that skipped ahead
+      // could otherwise wait on a slot whose previous phase is still pending -- a parity
+      // wait cannot tell the two phases apart, it would read the slot early and arrive on
+      // the wrong phase of `empty` (a hang on K = 2^20 scalar steps)
       tc::mbar_wait(&full[cur], cph);
+      if (!mine) continue;
       const R* st = st_base + cur * stage_elems;
       for (int itr = 0; itr < iters; ++itr) {
         const int kk = (itr * 32 + lane) * VEC;

@@ -147,5 +147,150 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __
         }
       }
 }
+
+// ----------------------------------------------------------- DMMA, gathered ----
+// The same GEMM reading the raw operands (interleaved complex128, any stored index order)
+// straight from the producing steps: the permutation to matricised form is folded into
+// the cp.async tile loads through GroupMap offset tables (as the small path does), so the
+// step has no pack pass (configs[3]: the planar packs were 28% of an amplitude).  Per CTA
+// the 64 row offsets of A and of B are computed once into shared memory; per stage each
+// thread gathers 16-byte complex elements, row-fastest or K-fastest along whichever is
+// contiguous in the operand's stored layout (kfast flags, chosen on the host) so a warp's
+// requests stay coalesced.  Tiles are interleaved [row][k] complex in shared memory with
+// the 16-byte column XOR-swizzled by (row & 7): the DMMA fragment loads (8 rows x 4 k per
+// warp, one LDS.128 = re + im) are conflict-free.
+struct GatherMaps {
+  GroupMap Ab, Am, Ak, Bb, Bn, Bk;
+  int32_t a_node, b_node;
+  int32_t a_kfast, b_kfast;
+};
+constexpr int G_STAGE = 2 * BM * BK;                      // complex128 per stage (A and B tiles)
+constexpr int G_KTAB = 1024;                              // K offsets tabulated per CTA up to this K
+constexpr int G_SMEM = STAGES * G_STAGE * 16 + 2 * BM * 8 + 2 * G_KTAB * 8;  // + row / K offsets
+
+__global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const GatherMaps gm_, const int64_t* __restrict__ tab,
+                                                                    void* const* __restrict__ ptrs, int32_t c_node,
+                                                                    int32_t M, int32_t N, int32_t K) {
+  extern __shared__ __align__(16) double2 smz[];
+  int64_t* rowA = reinterpret_cast<int64_t*>(smz + STAGES * G_STAGE);
+  int64_t* rowB = rowA + BM;
+  int64_t* kA = rowB + BM;                      // K offsets of A and B (K <= G_KTAB)
+  int64_t* kB = kA + G_KTAB;
+  const bool ktab = K <= G_KTAB;
+  if (ktab)
+    for (int k = threadIdx.x; k < K; k += THREADS) {
+      kA[k] = gmap(tab, gm_.Ak, k);
+      kB[k] = gmap(tab, gm_.Bk, k);
+    }
+  const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int group = pid / (GROUP_M * n_tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gmr = min(n_tiles_m - first_m, GROUP_M);
+  const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gmr;
+  const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gmr;
+  const int b = blockIdx.z;
+  const double2* __restrict__ A = reinterpret_cast<const double2*>(ptrs[gm_.a_node]);
+  const double2* __restrict__ B = reinterpret_cast<const double2*>(ptrs[gm_.b_node]);
+  if (threadIdx.x < BM) {
+    const int r = m_blk * BM + threadIdx.x;
+    rowA[threadIdx.x] = r < M ? gmap(tab, gm_.Ab, b) + gmap(tab, gm_.Am, r) : -1;
+  } else if (threadIdx.x < 2 * BM) {
+    const int r = n_blk * BN + threadIdx.x - BM;
+    rowB[threadIdx.x - BM] = r < N ? gmap(tab, gm_.Bb, b) + gmap(tab, gm_.Bn, r) : -1;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;   // 8 warps of 32 x 16
+  const int g = lane >> 2, t = lane & 3;
+
+  auto load_stage = [&](int stage, int k0) {
+    double2* st = smz + stage * G_STAGE;
+    // 2 operands x 64 rows x 16 k = 2048 complex, 8 per thread
+#pragma unroll
+    for (int i = 0; i < 2048 / THREADS; ++i) {
+      const int c = threadIdx.x + i * THREADS;
+      const int op = c >> 10, e = c & 1023;
+      const bool kf = op ? gm_.b_kfast : gm_.a_kfast;
+      const int row = kf ? e >> 4 : e & 63;
+      const int kk = kf ? e & 15 : e >> 6;
+      const int gk = k0 + kk;
+      const int64_t ro = op ? rowB[row] : rowA[row];
+      const bool valid = ro >= 0 && gk < K;
+      const double2* base = op ? B : A;
+      const double2* src = !valid ? base
+                           : base + ro + (ktab ? (op ? kB[gk] : kA[gk]) : gmap(tab, op ? gm_.Bk : gm_.Ak, gk));
+      cp_async16(st + op * BM * BK + row * BK + (kk ^ (row & 7)), src, valid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  double cr[2][2][4], ci[2][2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { cr[i][j][r] = 0.0; ci[i][j][r] = 0.0; }
+
+  const int nk = (K + BK - 1) / BK;
+#pragma unroll
+  for (int p = 0; p < STAGES - 1; ++p) {
+    if (p < nk) load_stage(p, p * BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();
+    if (kc + STAGES - 1 < nk) load_stage((kc + STAGES - 1) % STAGES, (kc + STAGES - 1) * BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const double2* sA = smz + (kc % STAGES) * G_STAGE;
+    const double2* sB = sA + BM * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[2][2], ai[2][2], nai[2][2], br[2], bi[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r0 = wm + i * 16 + g;
+        const double2 v0 = sA[r0 * BK + ((kk + t) ^ (r0 & 7))];
+        const double2 v1 = sA[(r0 + 8) * BK + ((kk + t) ^ ((r0 + 8) & 7))];
+        ar[i][0] = v0.x; ai[i][0] = v0.y; ar[i][1] = v1.x; ai[i][1] = v1.y;
+        nai[i][0] = -ai[i][0];
+        nai[i][1] = -ai[i][1];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n0 = wn + j * 8 + g;
+        const double2 w = sB[n0 * BK + ((kk + t) ^ (n0 & 7))];
+        br[j] = w.x;
+        bi[j] = w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
+          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
+          dmma(ci[i][j], ar[i][0], ar[i][1], bi[j]);
+          dmma(ci[i][j], ai[i][0], ai[i][1], br[j]);
+        }
+    }
+  }
+  double2* C = reinterpret_cast<double2*>(ptrs[c_node]) + (int64_t)b * M * (int64_t)N;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = m_blk * BM + wm + i * 16 + g + 8 * h;
+        const int col = n_blk * BN + wn + j * 8 + 2 * t;
+        if (row < M && col < N) {
+          double2* cp = C + (int64_t)row * N + col;
+          cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
+          if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
+        }
+      }
+}
 }  // namespace zg
 }  // namespace tnd

@@ -254,7 +254,18 @@ struct TcStep {
   CUtensorMap ta, tb;
   CUtensorMap tc;                 // C [b * M_c + row][N] complex64 for TMA stores (pair kernels)
   double flops;
+  bool gather = false;            // K_DMMA: operands gathered by the GEMM (no pack pass)
+  tnd::zg::GatherMaps gmaps{};
 };
+
+// TN_DMMA_GATHER=0: complex128 tensor-core steps pack their operands first (A/B switch)
+bool dmma_gather_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("TN_DMMA_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 // profiling marks: an event recorded before each kernel class (0 small, 1 pack, 2 gemm,
 // 3 reduce, 4 other) and its kernel (TN_K_*, tn_profile.k_*); time between consecutive
@@ -314,6 +325,18 @@ int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_b
 
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                  Marks* mk) {
+  const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
+                        (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
+  dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
+  if (t.gather) {
+    ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel, tnd::zg::G_SMEM);
+    if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma gather", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    tnd::zg::zgemm_dmma_gather_kernel<<<grid, tnd::zg::THREADS, tnd::zg::G_SMEM, st>>>(
+        t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+    g_launches++;
+    CK(cudaGetLastError());
+    return;
+  }
   ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_kernel, tnd::zg::SMEM);
   if (mk) mk->mark(st, 1, TN_K_PACK_PLANAR, profile_dump_ms() >= 0 ? shape_tag("f64 pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
   for (const PackDesc* d : {&t.px, &t.py}) {
@@ -323,9 +346,6 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
     g_launches++;
   }
   if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
-  const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
-                        (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
-  dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
   tnd::zg::zgemm_dmma_kernel<<<grid, tnd::zg::THREADS, tnd::zg::SMEM, st>>>(
       reinterpret_cast<const double*>(arena + t.x_off), reinterpret_cast<const double*>(arena + t.y_off), ptrs_d,
       t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
@@ -801,6 +821,30 @@ std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& b
   return k;
 }
 
+// complex128 tensor-core step reading its raw operands (zgemm_dmma_gather_kernel): offset
+// tables of the batch / free / contracted groups of X and Y in their stored layouts, and
+// which group holds each operand's stride-1 index (the gather's fast direction)
+void set_gather_maps(TcStep& t, TabPool& pool, int X, const NodeLayout& LX, int Y, const NodeLayout& LY,
+                     const std::vector<int>& batch, const std::vector<int>& fx, const std::vector<int>& fy,
+                     const std::vector<int>& kord, const std::vector<int>& l2) {
+  if (!dmma_gather_enabled()) return;
+  t.gather = true;
+  auto& g = t.gmaps;
+  g.Ab = pool.add(group_of(batch, LX, l2));
+  g.Am = pool.add(group_of(fx, LX, l2));
+  g.Ak = pool.add(group_of(kord, LX, l2));
+  g.Bb = pool.add(group_of(batch, LY, l2));
+  g.Bn = pool.add(group_of(fy, LY, l2));
+  g.Bk = pool.add(group_of(kord, LY, l2));
+  g.a_node = X;
+  g.b_node = Y;
+  auto kfast = [&](const NodeLayout& L) {
+    return !L.inds.empty() && std::count(kord.begin(), kord.end(), L.inds.back()) > 0;
+  };
+  g.a_kfast = kfast(LX);
+  g.b_kfast = kfast(LY);
+}
+
 // decide the path of a step (TC only for complex64 GEMM-shaped steps)
 bool want_tc(int dtype, int nb, int m, int n, int k) {
   if (dtype == TN_C128)   // DMMA tiles of 64 x 64 complex, K staged 16 at a time
@@ -848,6 +892,7 @@ void finish_cuda_core(TcStep& t, int dtype, int kind) {
   }
 }
 int64_t pack_bytes(const TcStep& t, int rows_bits) {
+  if (t.gather) return 16;                       // no pack buffer
   if (t.kind != K_TC) return int64_t(t.esz) << (t.nb_bits + rows_bits + t.k_lo);
   // 4 fp16 planes + one fp32 scale per row and 128-wide K chunk (+ slack: the GEMM's
   // scale copies read whole 128-row / BN-column tiles)
@@ -983,7 +1028,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? 3 : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
+        k += t.kind == K_DMMA ? (t.gather ? 1 : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
@@ -1184,6 +1229,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord, bool
       fx = slab_k_order(fx, L[X], l2, t.n_mslabs);
       t.px = make_pack(pool, X, L[X], cl.batch, fx, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, Y, L[Y], cl.batch, fy, kord, l2, planes, t.k_lo, &t.slab_y);
+      if (t.kind == K_DMMA) set_gather_maps(t, pool, X, L[X], Y, L[Y], cl.batch, fx, fy, kord, l2);
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       if (t.kind == K_TC || t.kind == K_DMMA) P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -1347,7 +1393,8 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord, bool
       bool slabbed = false;
       if (kind[pk]) {
         const auto& pt = P.tcs[big_index[pk]];
-        slabbed = pt.n_slabs > 1 || pt.n_mslabs > 1;
+        // (a gathering DMMA step reads its raw operands in its GEMM phase too)
+        slabbed = pt.n_slabs > 1 || pt.n_mslabs > 1 || pt.gather;
       }
       hi = 2 * step_pos[pk] + ((kind[pk] && !slabbed) ? 0 : 1);
       // the frontier of the prologue stays while the slices run
@@ -1554,7 +1601,7 @@ void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
           pr.k_bytes[kc] += b;
           pr.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
         } else {
-          const double pb = (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
+          const double pb = t.gather ? 0.0 : (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
           pr.n_gemm += t.n_slabs * t.n_mslabs;
           pr.n_pack += t.n_mslabs - 1;
           pr.flops_gemm += t.flops;
@@ -2127,6 +2174,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       const std::vector<int> kord = slab_k_order(cl.contr, mx >= my ? LX : LY, l2, t.n_slabs);
       t.px = make_pack(pool, 0, LX, batch, g1, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, 1, LY, batch, g2, kord, l2, planes, t.k_lo, &t.slab_y);
+      if (t.kind == K_DMMA) set_gather_maps(t, pool, 0, LX, 1, LY, batch, g1, g2, kord, l2);
       size_t xb = (size_t)pack_bytes(t, t.kind == K_TC ? t.m_lo : mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);

@@ -1,0 +1,10 @@
+# DMMA gather: complex128 tests, config 3 bench with and without the gather (A/B)
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 900 python -m pytest tests/test_gpu.py -x -q -m gpu -k "complex128 or config3 or iqp or config0 or degenerate or lanes or dmma" 2>&1 | tail -3
+for v in 0 1 0 1; do
+  TN_DMMA_GATHER=$v timeout 600 python bench.py --config 3 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/b3_g$v.json 2> gpurun_out/b3_g$v.err
+  python -c "
+import json; d=json.load(open('gpurun_out/b3_g$v.json'))
+print('gather=$v', round(d['ms_per_step'],3), 'ms/amp', round(d['amplitudes_per_s'],1), 'amp/s lanes', d['amplitudes_per_s_lanes']['value'] if d.get('amplitudes_per_s_lanes') else None, {k: round(v['ms'],3) for k, v in d['kernels'].items()})"
+done

@@ -257,6 +257,8 @@ SKINNY_CASES = [
     (0, 4, 3, 16, None),      # the configs[4] (4, 3, 26) K-slab shape at K = 65536 (8 groups of 4 x 4)
     (0, 4, 4, 12, 9),         # M = N = 16: 16 groups -> items on halves of X's rows, permuted
     (3, 1, 2, 10, 1),         # batch 8, one 2 x 4 group: 8 warps share its stage iterations
+    (0, 0, 0, 20, None),      # configs[3]'s scalar K = 2^20 step: 16 warps take one group's stages in turn
+    (10, 4, 4, 7, 2),         # configs[3]'s batched skinny step
 ]
 WIDE_CASES = [
     (0, 7, 9, 3, None),       # 128 x 512 outputs, K = 8
