@@ -593,6 +593,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
+    # stdout carries exactly one JSON line: Python's prints go to the original stdout, while
+    # file descriptor 1 (native libraries: NCCL's version banner under torchrun) goes to stderr
+    real_out = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(real_out, "w", buffering=1)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

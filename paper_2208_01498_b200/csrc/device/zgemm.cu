@@ -164,17 +164,25 @@ struct GatherMaps {
   int32_t a_node, b_node;
   int32_t a_kfast, b_kfast;
 };
-constexpr int G_STAGE = 2 * BM * BK;                      // complex128 per stage (A and B tiles)
 constexpr int G_KTAB = 1024;                              // K offsets tabulated per CTA up to this K
-constexpr int G_SMEM = STAGES * G_STAGE * 16 + 2 * BM * 8 + 2 * G_KTAB * 8;  // + row / K offsets
+// tiles of 64 x BNT complex (BNT = 64, or 32 when a step's 64-wide tiles would leave a
+// partial last wave: configs[3]'s dominant step, 1024 tiles = 3.46 waves of 296 slots)
+template <int BNT>
+__host__ __device__ constexpr int g_stage() { return (BM + BNT) * BK; }      // complex128 per stage (A and B tiles)
+template <int BNT>
+__host__ __device__ constexpr int g_smem() { return STAGES * g_stage<BNT>() * 16 + (BM + BNT) * 8 + 2 * G_KTAB * 8; }
 
+template <int BNT>
 __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const GatherMaps gm_, const int64_t* __restrict__ tab,
                                                                     void* const* __restrict__ ptrs, int32_t c_node,
                                                                     int32_t M, int32_t N, int32_t K) {
+  constexpr int G_STAGE = g_stage<BNT>();
+  constexpr int WN = BNT / 16, WM = 8 / WN;              // warp grid (N x M), warp tile 16 x (BM / WM)
+  constexpr int MI = BM / WM / 16;                        // 16-row fragments per warp
   extern __shared__ __align__(16) double2 smz[];
   int64_t* rowA = reinterpret_cast<int64_t*>(smz + STAGES * G_STAGE);
   int64_t* rowB = rowA + BM;
-  int64_t* kA = rowB + BM;                      // K offsets of A and B (K <= G_KTAB)
+  int64_t* kA = rowB + BNT;                     // K offsets of A and B (K <= G_KTAB)
   int64_t* kB = kA + G_KTAB;
   const bool ktab = K <= G_KTAB;
   if (ktab)
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
       kA[k] = gmap(tab, gm_.Ak, k);
       kB[k] = gmap(tab, gm_.Bk, k);
     }
-  const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BN - 1) / BN;
+  const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BNT - 1) / BNT;
   const int pid = blockIdx.x;
   const int group = pid / (GROUP_M * n_tiles_n);
   const int first_m = group * GROUP_M;
@@ -195,25 +203,26 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
   if (threadIdx.x < BM) {
     const int r = m_blk * BM + threadIdx.x;
     rowA[threadIdx.x] = r < M ? gmap(tab, gm_.Ab, b) + gmap(tab, gm_.Am, r) : -1;
-  } else if (threadIdx.x < 2 * BM) {
-    const int r = n_blk * BN + threadIdx.x - BM;
+  } else if (threadIdx.x < BM + BNT) {
+    const int r = n_blk * BNT + threadIdx.x - BM;
     rowB[threadIdx.x - BM] = r < N ? gmap(tab, gm_.Bb, b) + gmap(tab, gm_.Bn, r) : -1;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;   // 8 warps of 32 x 16
+  const int wm = (warp / WN) * (BM / WM), wn = (warp % WN) * 16;
   const int g = lane >> 2, t = lane & 3;
 
   auto load_stage = [&](int stage, int k0) {
     double2* st = smz + stage * G_STAGE;
-    // 2 operands x 64 rows x 16 k = 2048 complex, 8 per thread
+    // (64 + BNT) rows x 16 k complex: A then B, (64 + BNT) * 16 / 256 per thread
 #pragma unroll
-    for (int i = 0; i < 2048 / THREADS; ++i) {
+    for (int i = 0; i < (BM + BNT) * BK / THREADS; ++i) {
       const int c = threadIdx.x + i * THREADS;
-      const int op = c >> 10, e = c & 1023;
+      const int op = c >= BM * BK, e = op ? c - BM * BK : c;
+      const int rows = op ? BNT : BM;
       const bool kf = op ? gm_.b_kfast : gm_.a_kfast;
-      const int row = kf ? e >> 4 : e & 63;
-      const int kk = kf ? e & 15 : e >> 6;
+      const int row = kf ? e >> 4 : e & (rows - 1);
+      const int kk = kf ? e & 15 : e / rows;
       const int gk = k0 + kk;
       const int64_t ro = op ? rowB[row] : rowA[row];
       const bool valid = ro >= 0 && gk < K;
@@ -225,9 +234,9 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  double cr[2][2][4], ci[2][2][4];
+  double cr[MI][2][4], ci[MI][2][4];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -248,9 +257,9 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
     const double2* sB = sA + BM * BK;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double ar[2][2], ai[2][2], nai[2][2], br[2], bi[2];
+      double ar[MI][2], ai[MI][2], nai[MI][2], br[2], bi[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < MI; ++i) {
         const int r0 = wm + i * 16 + g;
         const double2 v0 = sA[r0 * BK + ((kk + t) ^ (r0 & 7))];
         const double2 v1 = sA[(r0 + 8) * BK + ((kk + t) ^ ((r0 + 8) & 7))];
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
         bi[j] = w.y;
       }
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
@@ -278,13 +287,13 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
   }
   double2* C = reinterpret_cast<double2*>(ptrs[c_node]) + (int64_t)b * M * (int64_t)N;
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int row = m_blk * BM + wm + i * 16 + g + 8 * h;
-        const int col = n_blk * BN + wn + j * 8 + 2 * t;
+        const int col = n_blk * BNT + wn + j * 8 + 2 * t;
         if (row < M && col < N) {
           double2* cp = C + (int64_t)row * N + col;
           cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};

@@ -323,16 +323,36 @@ int gemm_class(const TcStep& t) {
 // bytes of the 4 fp16 planes of a packed complex64 operand (its chunk scales follow)
 int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_bits + d.k_bits); }
 
+// 64 x 32 tiles for a gathered DMMA step (TN_DMMA_BN=32, an experiment switch): meant to
+// fill the partial last wave of 64 x 64 tiles (configs[3]'s dominant step: 1024 tiles =
+// 3.46 waves of 296 slots), but the halved warp tile (one 16-row fragment per warp) costs
+// more than the tail: configs[3] 1.92 -> 1.96 ms per amplitude (measured), so 64 wide
+bool dmma_bn32(const TcStep&) {
+  static const bool v = [] {
+    const char* e = std::getenv("TN_DMMA_BN");
+    return e && std::atoi(e) == 32;
+  }();
+  return v;
+}
+
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                  Marks* mk) {
   const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
                         (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
   if (t.gather) {
-    ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel, tnd::zg::G_SMEM);
     if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma gather", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
-    tnd::zg::zgemm_dmma_gather_kernel<<<grid, tnd::zg::THREADS, tnd::zg::G_SMEM, st>>>(
-        t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+    if (dmma_bn32(t)) {
+      const int64_t tiles32 = (((int64_t(1) << t.n_bits) + 31) / 32) * (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
+      ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<32>, tnd::zg::g_smem<32>());
+      tnd::zg::zgemm_dmma_gather_kernel<32><<<dim3((unsigned)tiles32, 1, 1u << t.nb_bits), tnd::zg::THREADS,
+                                              tnd::zg::g_smem<32>(), st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+    } else {
+      ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<64>, tnd::zg::g_smem<64>());
+      tnd::zg::zgemm_dmma_gather_kernel<64><<<grid, tnd::zg::THREADS, tnd::zg::g_smem<64>(), st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+    }
     g_launches++;
     CK(cudaGetLastError());
     return;
