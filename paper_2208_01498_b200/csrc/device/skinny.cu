@@ -483,9 +483,11 @@ __global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_
 // CTAs running together share Y columns in L2.  Accumulation in the plan's type: fp32 FMA
 // for complex64 (K <= 16 terms: the fp32-path bound of DESIGN.md "Tolerances"; fp64 here
 // ran at the FP64 pipe's ~12 TFLOP/s, 4x slower than writing C), fp64 for complex128.
+// KMAX = K (a template argument): the Y row lives in K-sized register arrays, so short-K
+// steps keep the occupancy (the 16-wide arrays held 128 registers at any K).
 constexpr int WD_THREADS = 256, WD_TM = 32, WD_MAXK = 16;
 
-template <typename R, int CPT>
+template <typename R, int CPT, int KMAX>
 __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ X, const R* __restrict__ Y,
                                                           void* const* __restrict__ ptrs, int32_t c_node,
                                                           int32_t m_bits, int32_t n_bits, int32_t k_bits,
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
   // CPT adjacent columns per thread (2 for complex64: each broadcast X load serves two
   // outputs and each thread stores 16 bytes)
   using C2 = typename cplx_t<R>::type;
-  __shared__ __align__(16) R xs[2][WD_TM][WD_MAXK];
+  __shared__ __align__(16) R xs[2][WD_TM][WD_MAXK];  // (rows of KMAX <= WD_MAXK)
   C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
   const int64_t M = int64_t(1) << m_bits, N = int64_t(1) << n_bits;
   const int K = 1 << k_bits;
@@ -516,12 +518,12 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
     }
     __syncthreads();
     if (n >= N || rg >= groups) continue;
-    R yr[CPT][WD_MAXK], yi[CPT][WD_MAXK];
+    R yr[CPT][KMAX], yi[CPT][KMAX];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       if (K % V == 0) {
 #pragma unroll
-        for (int q = 0; q < WD_MAXK / V; ++q) {
+        for (int q = 0; q < KMAX / V; ++q) {
           if (q * V < K) {
             R vr[V], vi[V];
             *reinterpret_cast<float4*>(vr) = __ldg(reinterpret_cast<const float4*>(yb + (n + c) * K) + q);
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < WD_MAXK; ++k)
+        for (int k = 0; k < KMAX; ++k)
           if (k < K) { yr[c][k] = __ldg(yb + (n + c) * K + k); yi[c][k] = __ldg(yb + (N + n + c) * K + k); }
       }
     }
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
       for (int c = 0; c < CPT; ++c) { re[c] = 0; im[c] = 0; }
       if (K % V == 0) {       // the row of X as 16-byte broadcast loads (the LDS count bounded this loop)
 #pragma unroll
-        for (int q = 0; q < WD_MAXK / V; ++q) {
+        for (int q = 0; q < KMAX / V; ++q) {
           if (q * V < K) {
             R xr[V], xi[V];
             *reinterpret_cast<float4*>(xr) = *reinterpret_cast<const float4*>(&xs[0][i][q * V]);
@@ -561,7 +563,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < WD_MAXK; ++k) {
+        for (int k = 0; k < KMAX; ++k) {
           if (k < K) {
             const R ar = xs[0][i][k], ai = xs[1][i][k];
 #pragma unroll

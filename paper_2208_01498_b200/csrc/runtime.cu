@@ -510,14 +510,15 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       const int64_t tm = std::min(tnd::WD_TM, 1 << t.m_bits), tn = int64_t(tnd::WD_THREADS) * (two ? 2 : 1);
       const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits)) / tm * (((int64_t(1) << t.n_bits) + tn - 1) / tn);
       const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
+#define TN_WIDE(CPT, KB)                                                                                    \
+  if (t.k_bits == KB)                                                                                       \
+    tnd::wide_kernel<R, CPT, 1 << KB><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, \
+                                                                         t.n_bits, t.k_bits, tiles);
       if constexpr (sizeof(R) == 4) {
-        if (two)
-          tnd::wide_kernel<R, 2><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits,
-                                                                    t.k_bits, tiles);
+        if (two) { TN_WIDE(2, 0) TN_WIDE(2, 1) TN_WIDE(2, 2) TN_WIDE(2, 3) TN_WIDE(2, 4) }
       }
-      if (!two)
-        tnd::wide_kernel<R, 1><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits,
-                                                                  t.k_bits, tiles);
+      if (!two) { TN_WIDE(1, 0) TN_WIDE(1, 1) TN_WIDE(1, 2) TN_WIDE(1, 3) TN_WIDE(1, 4) }
+#undef TN_WIDE
       g_launches++;
     }
   }
