@@ -211,9 +211,10 @@ int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_be
  * runs its prologue; tn_contract_prepared then ADDS the slices [slice_begin, slice_end)
  * of that bitstring to amp_dev (device complex128).  prof == NULL: CUDA-graph replay;
  * otherwise eager launches with CUDA events, prof (host) receives the pass's profile as
- * in tn_contract_profiled.  Any other contraction call on the plan (or on lane 0 through
- * tn_amplitudes) in between invalidates the prepared state; the caller orders the calls
- * on one stream. */
+ * in tn_contract_profiled.  Any other contraction call on the plan (tn_contract*,
+ * tn_amplitudes) in between invalidates the prepared state: tn_contract_prepared then
+ * fails with TN_EINVAL (as it does before any tn_prepare) on plans that have a prologue.
+ * The caller orders the calls on one stream. */
 int tn_prepare(tn_plan plan, const uint8_t* bits_dev, void* stream, tn_profile* prof);
 int tn_contract_prepared(tn_plan plan, int64_t slice_begin, int64_t slice_end, void* amp_dev, void* stream,
                          tn_profile* prof);

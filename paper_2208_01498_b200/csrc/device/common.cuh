@@ -30,6 +30,15 @@ struct SmallStep {
   GroupMap Ab, Am, Ak, Bb, Bk, Bn;
 };
 
+// Offset tables of a step whose kernel reads its raw operands (no pack pass): batch /
+// free / contracted groups of A (rows M) and B (rows N) in their stored layouts, the
+// operands' node ids, and whether each operand's stride-1 index is a contracted one.
+struct GatherMaps {
+  GroupMap Ab, Am, Ak, Bb, Bn, Bk;
+  int32_t a_node, b_node;
+  int32_t a_kfast, b_kfast;
+};
+
 template <typename T> struct cplx_t;
 template <> struct cplx_t<float> { using type = float2; };
 template <> struct cplx_t<double> { using type = double2; };

@@ -487,18 +487,31 @@ __global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_
 // steps keep the occupancy (the 16-wide arrays held 128 registers at any K).
 constexpr int WD_THREADS = 256, WD_TM = 32, WD_MAXK = 16;
 
-template <typename R, int CPT, int KMAX>
+// GATHER: X and Y are the raw operands (interleaved complex, any stored index order), read
+// through the step's offset tables `gm` (no planar pack pass; the tables' K offsets go to
+// shared memory once per CTA); else X / Y are the planar packed operands.
+template <typename R, int CPT, int KMAX, bool GATHER>
 __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ X, const R* __restrict__ Y,
                                                           void* const* __restrict__ ptrs, int32_t c_node,
                                                           int32_t m_bits, int32_t n_bits, int32_t k_bits,
-                                                          int64_t n_tiles) {
+                                                          int64_t n_tiles, const GatherMaps gm,
+                                                          const int64_t* __restrict__ tab) {
   // CPT adjacent columns per thread (2 for complex64: each broadcast X load serves two
   // outputs and each thread stores 16 bytes)
   using C2 = typename cplx_t<R>::type;
   __shared__ __align__(16) R xs[2][WD_TM][WD_MAXK];  // (rows of KMAX <= WD_MAXK)
+  __shared__ int64_t kofs[2][KMAX];                  // GATHER: K offsets of X and Y
   C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
   const int64_t M = int64_t(1) << m_bits, N = int64_t(1) << n_bits;
   const int K = 1 << k_bits;
+  const C2* __restrict__ Xc = GATHER ? reinterpret_cast<const C2*>(ptrs[gm.a_node]) : nullptr;
+  const C2* __restrict__ Yc = GATHER ? reinterpret_cast<const C2*>(ptrs[gm.b_node]) : nullptr;
+  if constexpr (GATHER) {
+    if (threadIdx.x < K) {
+      kofs[0][threadIdx.x] = gmap(tab, gm.Ak, threadIdx.x);
+      kofs[1][threadIdx.x] = gmap(tab, gm.Bk, threadIdx.x);
+    }
+  }
   const int tm = (int)(M < WD_TM ? M : WD_TM);
   constexpr int TN = WD_THREADS * CPT;
   const int64_t mt = M / tm, ncb = (N + TN - 1) / TN;
@@ -512,16 +525,34 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
     const R* __restrict__ xb = X + b * 2 * M * K;
     const R* __restrict__ yb = Y + b * 2 * N * K;
     __syncthreads();                                 // the previous tile's xs reads are done
-    for (int e = threadIdx.x; e < 2 * tm * K; e += WD_THREADS) {
-      const int p = e / (tm * K), i = (e / K) % tm, k = e % K;
-      xs[p][i][k] = xb[(p * M + m0 + i) * K + k];
+    if constexpr (GATHER) {
+      const int64_t xbo = gmap(tab, gm.Ab, b);
+      for (int e = threadIdx.x; e < tm * K; e += WD_THREADS) {
+        const int i = e / K, k = e % K;
+        const C2 v = Xc[xbo + gmap(tab, gm.Am, m0 + i) + kofs[0][k]];
+        xs[0][i][k] = v.x;
+        xs[1][i][k] = v.y;
+      }
+    } else {
+      for (int e = threadIdx.x; e < 2 * tm * K; e += WD_THREADS) {
+        const int p = e / (tm * K), i = (e / K) % tm, k = e % K;
+        xs[p][i][k] = xb[(p * M + m0 + i) * K + k];
+      }
     }
     __syncthreads();
     if (n >= N || rg >= groups) continue;
     R yr[CPT][KMAX], yi[CPT][KMAX];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-      if (K % V == 0) {
+      if constexpr (GATHER) {
+        const int64_t yo = gmap(tab, gm.Bb, b) + gmap(tab, gm.Bn, n + c);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+          const C2 v = Yc[yo + kofs[1][k]];
+          yr[c][k] = v.x;
+          yi[c][k] = v.y;
+        }
+      } else if (K % V == 0) {
 #pragma unroll
         for (int q = 0; q < KMAX / V; ++q) {
           if (q * V < K) {

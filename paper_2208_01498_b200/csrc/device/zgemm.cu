@@ -159,11 +159,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __
 // requests stay coalesced.  Tiles are interleaved [row][k] complex in shared memory with
 // the 16-byte column XOR-swizzled by (row & 7): the DMMA fragment loads (8 rows x 4 k per
 // warp, one LDS.128 = re + im) are conflict-free.
-struct GatherMaps {
-  GroupMap Ab, Am, Ak, Bb, Bn, Bk;
-  int32_t a_node, b_node;
-  int32_t a_kfast, b_kfast;
-};
+using tnd::GatherMaps;
 constexpr int G_KTAB = 1024;                              // K offsets tabulated per CTA up to this K
 // tiles of 64 x BNT complex (BNT = 64, or 32 when a step's 64-wide tiles would leave a
 // partial last wave: configs[3]'s dominant step, 1024 tiles = 3.46 waves of 296 slots)

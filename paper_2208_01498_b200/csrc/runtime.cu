@@ -258,10 +258,18 @@ struct TcStep {
   tnd::zg::GatherMaps gmaps{};
 };
 
-// TN_DMMA_GATHER=0: complex128 tensor-core steps pack their operands first (A/B switch)
+// TN_DMMA_GATHER=0 / TN_WIDE_GATHER=0: complex128 tensor-core steps / wide steps pack
+// their operands first (A/B switches)
 bool dmma_gather_enabled() {
   static bool v = [] {
     const char* e = std::getenv("TN_DMMA_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+bool wide_gather_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("TN_WIDE_GATHER");
     return !(e && e[0] == '0');
   }();
   return v;
@@ -454,9 +462,11 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
   const R* Y = reinterpret_cast<const R*>(arena + t.y_off);
   const bool dump = profile_dump_ms() >= 0;
   for (int s = 0; s < t.n_slabs; ++s) {
-    if (mk) mk->mark(st, 1, TN_K_PACK_PLANAR, dump ? shape_tag("planar pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
-    pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
-    pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
+    if (!t.gather) {   // (gathered wide steps read their raw operands)
+      if (mk) mk->mark(st, 1, TN_K_PACK_PLANAR, dump ? shape_tag("planar pack", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+      pack(t.px, t.x_off, t.slab_x.empty() ? 0 : t.slab_x[s]);
+      pack(t.py, t.y_off, t.slab_y.empty() ? 0 : t.slab_y[s]);
+    }
     if (mk) mk->mark(st, 0, t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE,
                      dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
                                              t.k_bits) : "");
@@ -511,9 +521,14 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits)) / tm * (((int64_t(1) << t.n_bits) + tn - 1) / tn);
       const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
 #define TN_WIDE(CPT, KB)                                                                                    \
-  if (t.k_bits == KB)                                                                                       \
-    tnd::wide_kernel<R, CPT, 1 << KB><<<grid, tnd::WD_THREADS, 0, st>>>(X, Y, ptrs_d, t.c_node, t.m_bits, \
-                                                                         t.n_bits, t.k_bits, tiles);
+  if (t.k_bits == KB) {                                                                                     \
+    if (t.gather)                                                                                           \
+      tnd::wide_kernel<R, CPT, 1 << KB, true><<<grid, tnd::WD_THREADS, 0, st>>>(                           \
+          X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles, t.gmaps, tab_d);                     \
+    else                                                                                                    \
+      tnd::wide_kernel<R, CPT, 1 << KB, false><<<grid, tnd::WD_THREADS, 0, st>>>(                          \
+          X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles, t.gmaps, tab_d);                     \
+  }
       if constexpr (sizeof(R) == 4) {
         if (two) { TN_WIDE(2, 0) TN_WIDE(2, 1) TN_WIDE(2, 2) TN_WIDE(2, 3) TN_WIDE(2, 4) }
       }
@@ -848,7 +863,7 @@ std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& b
 void set_gather_maps(TcStep& t, TabPool& pool, int X, const NodeLayout& LX, int Y, const NodeLayout& LY,
                      const std::vector<int>& batch, const std::vector<int>& fx, const std::vector<int>& fy,
                      const std::vector<int>& kord, const std::vector<int>& l2) {
-  if (!dmma_gather_enabled()) return;
+  if (t.kind == K_DMMA ? !dmma_gather_enabled() : t.kind == K_WIDE ? !wide_gather_enabled() : true) return;
   t.gather = true;
   auto& g = t.gmaps;
   g.Ab = pool.add(group_of(batch, LX, l2));
@@ -978,6 +993,7 @@ struct tn_plan_s {
   int64_t frontier_bytes = 0;
   int64_t kernels_pro = 0;
   cudaGraphExec_t graph_pro = nullptr;
+  bool prepared = false;            // tn_prepare ran and no other contraction call since
   int64_t n_slices = 1;
   int slice_bits = 0;
   double flops = 0, tc_flops = 0;
@@ -1049,7 +1065,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? (t.gather ? 1 : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? 3 * t.n_slabs
+        k += t.kind == K_DMMA ? (t.gather ? 1 : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }
@@ -1250,7 +1266,7 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord, bool
       fx = slab_k_order(fx, L[X], l2, t.n_mslabs);
       t.px = make_pack(pool, X, L[X], cl.batch, fx, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, Y, L[Y], cl.batch, fy, kord, l2, planes, t.k_lo, &t.slab_y);
-      if (t.kind == K_DMMA) set_gather_maps(t, pool, X, L[X], Y, L[Y], cl.batch, fx, fy, kord, l2);
+      set_gather_maps(t, pool, X, L[X], Y, L[Y], cl.batch, fx, fy, kord, l2);   // DMMA / wide
       t.flops = 8.0 * std::ldexp(1.0, nb + ml + mr + kk);
       if (t.kind == K_TC || t.kind == K_DMMA) P.tc_flops += t.flops;
       L[c].inds = cl.batch;
@@ -1616,11 +1632,11 @@ void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
           pr.n_small += t.n_slabs;
           pr.flops_small += t.flops;
           pr.bytes_small += b;
-          pr.bytes_pack += 2.0 * t.esz * (ex + ey);
+          if (!t.gather) pr.bytes_pack += 2.0 * t.esz * (ex + ey);
           const int kc = t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE;
           pr.k_flops[kc] += t.flops;
           pr.k_bytes[kc] += b;
-          pr.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
+          if (!t.gather) pr.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
         } else {
           const double pb = t.gather ? 0.0 : (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
           pr.n_gemm += t.n_slabs * t.n_mslabs;
@@ -1708,6 +1724,8 @@ void run_prologue(tn_plan_s& P, cudaStream_t st) {
 // (tn_contract_prepared); otherwise copy it in and run the prologue first
 void run_slices(tn_plan_s& P, const uint8_t* bits, bool bits_on_device, int64_t s0, int64_t s1, cudaStream_t st) {
   if (s0 < 0 || s1 > P.n_slices || s0 > s1) throw Err(TN_EINVAL, "slice range out of bounds");
+  if (!bits && P.n_pro > 0 && !P.prepared) throw Err(TN_EINVAL, "tn_contract_prepared without tn_prepare");
+  if (bits) P.prepared = false;     // this call's prologue replaces the prepared bitstring
   CK(cudaSetDevice(P.device));
   if (bits && P.net->n_qubits > 0)
     CK(cudaMemcpyAsync(P.bits_d, bits, P.net->n_qubits, bits_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -1947,6 +1965,7 @@ int tn_contract_profiled(tn_plan p, const uint8_t* bits_dev, int64_t slice_begin
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaSetDevice(p->device));
     if (p->net->n_qubits > 0) CK(cudaMemcpyAsync(p->bits_d, bits_dev, p->net->n_qubits, cudaMemcpyDeviceToDevice, st));
+    p->prepared = false;
     set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
     CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
     profile_slices(*p, slice_begin, slice_end, st, *prof, true);
@@ -1968,6 +1987,7 @@ int tn_prepare(tn_plan p, const uint8_t* bits_dev, void* stream, tn_profile* pro
     } else {
       run_prologue(*p, st);
     }
+    p->prepared = true;
     CK(cudaGetLastError());
   });
 }
@@ -1980,6 +2000,7 @@ int tn_contract_prepared(tn_plan p, int64_t slice_begin, int64_t slice_end, void
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaSetDevice(p->device));
     if (prof) {
+      if (p->n_pro > 0 && !p->prepared) throw Err(TN_EINVAL, "tn_contract_prepared without tn_prepare");
       set_i64_kernel<<<1, 1, 0, st>>>(p->slice_d, slice_begin);
       CK(cudaMemsetAsync(p->amp_d, 0, 16, st));
       profile_slices(*p, slice_begin, slice_end, st, *prof, false);
@@ -1998,6 +2019,7 @@ int tn_amplitudes(tn_plan p, const uint8_t* bits, int32_t n_bits, double* amps, 
     cudaStream_t st = (cudaStream_t)stream;
     const int nq = p->net->n_qubits;
     CK(cudaSetDevice(p->device));
+    p->prepared = false;
     if (p->extra.empty() || n_bits < 2) {
       for (int j = 0; j < n_bits; ++j) {
         run_slices(*p, bits + (size_t)j * nq, false, 0, p->n_slices, st);
@@ -2195,7 +2217,7 @@ int tn_contract_pair(int32_t dtype, const void* A, int32_t rank_a, const int32_t
       const std::vector<int> kord = slab_k_order(cl.contr, mx >= my ? LX : LY, l2, t.n_slabs);
       t.px = make_pack(pool, 0, LX, batch, g1, kord, l2, planes, t.k_lo, &t.slab_x, t.m_lo);
       t.py = make_pack(pool, 1, LY, batch, g2, kord, l2, planes, t.k_lo, &t.slab_y);
-      if (t.kind == K_DMMA) set_gather_maps(t, pool, 0, LX, 1, LY, batch, g1, g2, kord, l2);
+      set_gather_maps(t, pool, 0, LX, 1, LY, batch, g1, g2, kord, l2);   // DMMA / wide
       size_t xb = (size_t)pack_bytes(t, t.kind == K_TC ? t.m_lo : mx), yb = (size_t)pack_bytes(t, my);
       size_t pb = (size_t)tc_partial_bytes(t);
       char* scratch = (char*)dalloc(xb + yb + pb + 3 * ALIGN);

@@ -181,6 +181,10 @@ def test_slice_reuse_prologue():
         plan.contract_prepared(0, ns, prof.data_ptr(), st)
         torch.cuda.synchronize()
         a_full, a_parts, a_prof = full.item(), parts.sum().item(), prof.item()
+        # another contraction call invalidates the prepared bitstring
+        plan.contract(x, 0, 1)
+        with pytest.raises(tb.TnError):
+            plan.contract_prepared(0, 1, prof.data_ptr(), st)
         assert abs(a_parts - a_full) <= 1e-12 * abs(a_full) and abs(a_prof - a_full) <= 1e-12 * abs(a_full)
         want = contract_tree(on, order.steps(), x)
         assert abs(a_full - want) <= 1e-5 * max(abs(want), 2.0 ** (-c.n / 2))
