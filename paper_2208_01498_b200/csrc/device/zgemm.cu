@@ -169,9 +169,12 @@ template <int BNT>
 __host__ __device__ constexpr int g_smem() { return STAGES * g_stage<BNT>() * 16 + (BM + BNT) * 8 + 2 * G_KTAB * 8; }
 
 template <int BNT>
+// ksplit = 2: blockIdx.y takes one half of K and the halves are ADDED to a zeroed C by
+// fp64 atomics -- two addends onto 0.0 commute exactly, so the result is deterministic
+// (fills the partial last wave of a step with few tiles)
 __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const GatherMaps gm_, const int64_t* __restrict__ tab,
                                                                     void* const* __restrict__ ptrs, int32_t c_node,
-                                                                    int32_t M, int32_t N, int32_t K) {
+                                                                    int32_t M, int32_t N, int32_t K, int32_t ksplit) {
   constexpr int G_STAGE = g_stage<BNT>();
   constexpr int WN = BNT / 16, WM = 8 / WN;              // warp grid (N x M), warp tile 16 x (BM / WM)
   constexpr int MI = BM / WM / 16;                        // 16-row fragments per warp
@@ -238,16 +241,17 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
 #pragma unroll
       for (int r = 0; r < 4; ++r) { cr[i][j][r] = 0.0; ci[i][j][r] = 0.0; }
 
-  const int nk = (K + BK - 1) / BK;
+  const int kbeg = ksplit > 1 ? (int)blockIdx.y * (K / ksplit) : 0;
+  const int nk = ((ksplit > 1 ? K / ksplit : K) + BK - 1) / BK;
 #pragma unroll
   for (int p = 0; p < STAGES - 1; ++p) {
-    if (p < nk) load_stage(p, p * BK);
+    if (p < nk) load_stage(p, kbeg + p * BK);
     else asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int kc = 0; kc < nk; ++kc) {
     asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
     __syncthreads();
-    if (kc + STAGES - 1 < nk) load_stage((kc + STAGES - 1) % STAGES, (kc + STAGES - 1) * BK);
+    if (kc + STAGES - 1 < nk) load_stage((kc + STAGES - 1) % STAGES, kbeg + (kc + STAGES - 1) * BK);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     const double2* sA = smz + (kc % STAGES) * G_STAGE;
     const double2* sB = sA + BM * BK;
@@ -292,10 +296,23 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
         const int col = n_blk * BNT + wn + j * 8 + 2 * t;
         if (row < M && col < N) {
           double2* cp = C + (int64_t)row * N + col;
-          cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
-          if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
+          if (ksplit > 1) {
+            atomicAdd(&cp[0].x, cr[i][j][2 * h]);
+            atomicAdd(&cp[0].y, ci[i][j][2 * h]);
+            if (col + 1 < N) { atomicAdd(&cp[1].x, cr[i][j][2 * h + 1]); atomicAdd(&cp[1].y, ci[i][j][2 * h + 1]); }
+          } else {
+            cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
+            if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
+          }
         }
       }
+}
+
+// zero the complex128 node c_node (n elements): the split-K DMMA accumulates into it
+__global__ void zero_node_kernel(void* const* __restrict__ ptrs, int32_t c_node, int64_t n) {
+  double2* C = reinterpret_cast<double2*>(ptrs[c_node]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    C[i] = double2{0.0, 0.0};
 }
 }  // namespace zg
 }  // namespace tnd

@@ -343,6 +343,23 @@ bool dmma_bn32(const TcStep&) {
   return v;
 }
 
+// split K in two for a gathered DMMA step whose 64 x 64 tiles leave most of a last wave idle
+// (2 CTAs per SM: 296 slots) and that keeps >= 8 K stages per half: an experiment switch
+// (TN_DMMA_KSPLIT=1), off by default -- measured slower on configs[3] (its DMMA 1.02 ->
+// 1.11 ms per amplitude: the zeroing pass, the fp64 atomics and the halved K per CTA cost
+// more than the 3.46-wave tail)
+int dmma_ksplit(const TcStep& t) {
+  static const bool on = [] {
+    const char* e = std::getenv("TN_DMMA_KSPLIT");
+    return e && e[0] == '1';
+  }();
+  if (!on || !t.gather || dmma_bn32(t) || t.k_bits < 8) return 1;
+  const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
+                        (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM) << t.nb_bits;
+  const int64_t slots = 296, rem = tiles % slots;
+  return (tiles < 4 * slots && rem != 0 && rem < slots * 3 / 4) ? 2 : 1;
+}
+
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
                  Marks* mk) {
   const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
@@ -350,16 +367,23 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
   if (t.gather) {
     if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma gather", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
+    const int ks = dmma_ksplit(t);
+    if (ks > 1) {
+      const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+      tnd::zg::zero_node_kernel<<<(unsigned)std::min<int64_t>((n_out + 255) / 256, 148 * 8), 256, 0, st>>>(
+          ptrs_d, t.c_node, n_out);
+      g_launches++;
+    }
     if (dmma_bn32(t)) {
       const int64_t tiles32 = (((int64_t(1) << t.n_bits) + 31) / 32) * (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
       ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<32>, tnd::zg::g_smem<32>());
-      tnd::zg::zgemm_dmma_gather_kernel<32><<<dim3((unsigned)tiles32, 1, 1u << t.nb_bits), tnd::zg::THREADS,
+      tnd::zg::zgemm_dmma_gather_kernel<32><<<dim3((unsigned)tiles32, ks, 1u << t.nb_bits), tnd::zg::THREADS,
                                               tnd::zg::g_smem<32>(), st>>>(
-          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, ks);
     } else {
       ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<64>, tnd::zg::g_smem<64>());
-      tnd::zg::zgemm_dmma_gather_kernel<64><<<grid, tnd::zg::THREADS, tnd::zg::g_smem<64>(), st>>>(
-          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits);
+      tnd::zg::zgemm_dmma_gather_kernel<64><<<dim3(grid.x, ks, grid.z), tnd::zg::THREADS, tnd::zg::g_smem<64>(), st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, ks);
     }
     g_launches++;
     CK(cudaGetLastError());
@@ -1065,7 +1089,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? (t.gather ? 1 : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
+        k += t.kind == K_DMMA ? (t.gather ? (dmma_ksplit(t) > 1 ? 2 : 1) : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }

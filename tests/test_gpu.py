@@ -317,6 +317,7 @@ DMMA_CASES = [
     (0, 5, 7, 3, 2),          # ragged M = 32, N = 128, K = 8, permuted
     (2, 7, 6, 9, 4),          # batch 4, K = 512 (32 stages), permuted
     (0, 9, 9, 6, None),       # 64 tiles
+    (6, 10, 6, 9, 5),         # configs[3]'s dominant step: 1024 tiles = 3.46 waves -> K split in 2 (fp64 atomics)
 ]
 
 
@@ -326,6 +327,27 @@ def test_pair_complex128_dmma_path(case):
     ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
     got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
     assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
+
+
+def test_pair_complex128_dmma_ksplit():
+    """The K-split DMMA variant (TN_DMMA_KSPLIT=1, child process): configs[3]'s dominant
+    shape, 1024 tiles = 3.46 waves, K halves added by fp64 atomics onto a zeroed C --
+    within the DMMA bound and bit-identical over two runs (two addends onto 0 commute)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+        import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
+        ia, ib, ic, dims = T._gemm_case(6, 10, 6, 9, 5)
+        got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=7)
+        assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
+        again, _, _ = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=7)
+        assert np.array_equal(got, again)
+        print('ok')
+    """)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env=dict(os.environ, TN_DMMA_KSPLIT="1"),
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_pair_tensor_core_k_slabs(monkeypatch):
