@@ -28,7 +28,10 @@ def _circuit(kind, seed):
     return random3d(7, int(rng.integers(8, 11)), seed, n_patches=1, patch=4), False
 
 
-@pytest.mark.parametrize("case", range(12))
+_SEEN = set()
+
+
+@pytest.mark.parametrize("case", range(24))
 def test_random_plans_match_oracle(case):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -46,6 +49,10 @@ def test_random_plans_match_oracle(case):
     assert co.steps() == osteps
     dtype = tb.TN_C128 if case % 2 else tb.TN_C64
     plan = tb.Plan(cn, co, dtype=dtype)
+    st = plan.steps()
+    _SEEN.update((int(p), dtype) for p in st[:, 0])
+    if plan.info()["flops_prologue"] > 0:
+        _SEEN.add(("reuse", dtype))
     bits = random_bitstrings(c.n, 3, case)
     got1 = plan.amplitudes(bits)
     plan.set_lanes(2)
@@ -55,3 +62,15 @@ def test_random_plans_match_oracle(case):
     for x, g in zip(bits, got1):
         want = contract_tree(on, osteps, x)
         assert abs(g - want) <= tol * max(abs(want), 2.0 ** (-c.n / 2)), (kind, tgt, dtype, g, want)
+
+
+def test_random_plans_covered_every_path():
+    """the random plans above went through the small and tensor-core paths and slice reuse in
+    both dtypes, and through the (gathering) wide kernel"""
+    if not _SEEN:
+        pytest.skip("random plans did not run")
+    for dt in (tb.TN_C64, tb.TN_C128):
+        for path in (tb.TN_PATH_SMALL, tb.TN_PATH_TC):
+            assert (path, dt) in _SEEN, (path, dt, sorted(map(str, _SEEN)))
+        assert ("reuse", dt) in _SEEN, dt
+    assert any((tb.TN_PATH_WIDE, dt) in _SEEN for dt in (tb.TN_C64, tb.TN_C128))
