@@ -330,6 +330,9 @@ def run_ours(args):
         os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (no version banner)
     if distributed:
         import torch.distributed as tdist
+        # ranks on one host share its cores for the order search (tn_find_order threads)
+        lws = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        os.environ.setdefault("TN_ORDER_THREADS", str(max(1, (os.cpu_count() or 1) // max(lws, 1))))
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <exception>
 #include <thread>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <numeric>
@@ -621,7 +622,11 @@ Order find_order(const Network& net, uint64_t seed, const OrderParams& p) {
       work[r] = sliced_work(net, o.steps, o.slices);
     }
   };
-  const int T = std::max(1, std::min<int>(R, (int)std::thread::hardware_concurrency()));
+  // host threads: all cores, or TN_ORDER_THREADS (bench.py sets it to the cores per rank
+  // when several ranks share a host); the choice does not depend on the thread count
+  int hw = (int)std::thread::hardware_concurrency();
+  if (const char* e = std::getenv("TN_ORDER_THREADS")) hw = std::atoi(e);
+  const int T = std::max(1, std::min<int>(R, hw));
   std::atomic<int> next{0};
   std::vector<std::exception_ptr> err(T);
   std::vector<std::thread> pool;
