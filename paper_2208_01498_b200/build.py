@@ -56,6 +56,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(s) + ".o")
         if force or _newer([src] + deps, obj):
             out = _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+                        *os.environ.get("TN_NVCC_EXTRA", "").split(),
                         "-Xcompiler", "-fPIC,-ffp-contract=off", *inc, "-c", src, "-o", obj])
             if verbose:
                 sys.stdout.write(out)

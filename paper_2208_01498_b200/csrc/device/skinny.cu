@@ -473,6 +473,11 @@ __global__ void skinny_reduce_kernel(const double2* __restrict__ partial, int32_
   }
 }
 
+// packed fp32 pair FMA (FFMA2: two fp32 lanes per instruction, half the issue slots of FFMA)
+__device__ __forceinline__ void fma2_(uint64_t& d, uint64_t a, uint64_t b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
 // ------------------------------------------------------------------- wide ----
 // C[b][m][n] = sum_k X[b][m][k] Y[b][n][k] with K <= WD_MAXK (16): a short contraction
 // onto a large output, bound by writing C.  A CTA covers rows [m0, m0 + tm) (tm <=
@@ -490,7 +495,9 @@ constexpr int WD_THREADS = 256, WD_TM = 32, WD_MAXK = 16;
 // GATHER: X and Y are the raw operands (interleaved complex, any stored index order), read
 // through the step's offset tables `gm` (no planar pack pass; the tables' K offsets go to
 // shared memory once per CTA); else X / Y are the planar packed operands.
-template <typename R, int CPT, int KMAX, bool GATHER>
+// F2 (complex64, CPT = 2, gathered): packed fp32 pair FMAs (FFMA2), 4 per k and row
+// instead of 8 FFMA.
+template <typename R, int CPT, int KMAX, bool GATHER, bool F2 = false>
 __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ X, const R* __restrict__ Y,
                                                           void* const* __restrict__ ptrs, int32_t c_node,
                                                           int32_t m_bits, int32_t n_bits, int32_t k_bits,
@@ -541,77 +548,117 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
     }
     __syncthreads();
     if (n >= N || rg >= groups) continue;
-    R yr[CPT][KMAX], yi[CPT][KMAX];
+    if constexpr (F2) {
+      // gathered Y entries are (re, im) register pairs: per column c, P += x_r (y_re, y_im)
+      // and Q += x_i (y_re, y_im) (broadcast X element), re = P.lo - Q.hi, im = P.hi + Q.lo
+      static_assert(sizeof(R) == 4 && CPT == 2 && GATHER, "FFMA2 wide: complex64, two columns, gathered");
+      uint64_t yp[CPT][KMAX];
+      const int64_t yb0 = gmap(tab, gm.Bb, b);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if constexpr (GATHER) {
-        const int64_t yo = gmap(tab, gm.Bb, b) + gmap(tab, gm.Bn, n + c);
+      for (int c = 0; c < CPT; ++c) {
+        const int64_t yo = yb0 + gmap(tab, gm.Bn, n + c);
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) {
-          const C2 v = Yc[yo + kofs[1][k]];
-          yr[c][k] = v.x;
-          yi[c][k] = v.y;
-        }
-      } else if (K % V == 0) {
-#pragma unroll
-        for (int q = 0; q < KMAX / V; ++q) {
-          if (q * V < K) {
-            R vr[V], vi[V];
-            *reinterpret_cast<float4*>(vr) = __ldg(reinterpret_cast<const float4*>(yb + (n + c) * K) + q);
-            *reinterpret_cast<float4*>(vi) = __ldg(reinterpret_cast<const float4*>(yb + (N + n + c) * K) + q);
-#pragma unroll
-            for (int u = 0; u < V; ++u) { yr[c][q * V + u] = vr[u]; yi[c][q * V + u] = vi[u]; }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-          if (k < K) { yr[c][k] = __ldg(yb + (n + c) * K + k); yi[c][k] = __ldg(yb + (N + n + c) * K + k); }
+        for (int k = 0; k < KMAX; ++k) yp[c][k] = *reinterpret_cast<const unsigned long long*>(Yc + yo + kofs[1][k]);
       }
-    }
-    C2* __restrict__ cp = C + (b * M + m0) * N + n;
-    for (int i = rg; i < tm; i += groups) {
-      R re[CPT], im[CPT];
+      C2* __restrict__ cp = C + (b * M + m0) * N + n;
+      for (int i = rg; i < tm; i += groups) {
+        uint64_t P[CPT] = {0, 0}, Q[CPT] = {0, 0};
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) { re[c] = 0; im[c] = 0; }
-      if (K % V == 0) {       // the row of X as 16-byte broadcast loads (the LDS count bounded this loop)
+        for (int q = 0; q < KMAX / 4; ++q) {
+          const float4 xr = *reinterpret_cast<const float4*>(&xs[0][i][q * 4]);
+          const float4 xi = *reinterpret_cast<const float4*>(&xs[1][i][q * 4]);
 #pragma unroll
-        for (int q = 0; q < KMAX / V; ++q) {
-          if (q * V < K) {
-            R xr[V], xi[V];
-            *reinterpret_cast<float4*>(xr) = *reinterpret_cast<const float4*>(&xs[0][i][q * V]);
-            *reinterpret_cast<float4*>(xi) = *reinterpret_cast<const float4*>(&xs[1][i][q * V]);
-#pragma unroll
-            for (int u = 0; u < V; ++u)
-#pragma unroll
-              for (int c = 0; c < CPT; ++c) {
-                re[c] = fma(xr[u], yr[c][q * V + u], re[c]);
-                re[c] = fma(-xi[u], yi[c][q * V + u], re[c]);
-                im[c] = fma(xr[u], yi[c][q * V + u], im[c]);
-                im[c] = fma(xi[u], yr[c][q * V + u], im[c]);
-              }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k) {
-          if (k < K) {
-            const R ar = xs[0][i][k], ai = xs[1][i][k];
+          for (int u = 0; u < 4; ++u) {
+            uint64_t a_r, a_i;
+            asm("mov.b64 %0, {%1,%1};" : "=l"(a_r) : "f"((&xr.x)[u]));
+            asm("mov.b64 %0, {%1,%1};" : "=l"(a_i) : "f"((&xi.x)[u]));
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-              re[c] = fma(ar, yr[c][k], re[c]);
-              re[c] = fma(-ai, yi[c][k], re[c]);
-              im[c] = fma(ar, yi[c][k], im[c]);
-              im[c] = fma(ai, yr[c][k], im[c]);
+              fma2_(P[c], a_r, yp[c][q * 4 + u]);
+              fma2_(Q[c], a_i, yp[c][q * 4 + u]);
             }
           }
         }
+        float p0r, p0i, q0r, q0i, p1r, p1i, q1r, q1i;
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(p0r), "=f"(p0i) : "l"(P[0]));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(q0r), "=f"(q0i) : "l"(Q[0]));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(p1r), "=f"(p1i) : "l"(P[1]));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(q1r), "=f"(q1i) : "l"(Q[1]));
+        *reinterpret_cast<float4*>(cp + (int64_t)i * N) = make_float4(p0r - q0i, p0i + q0r, p1r - q1i, p1i + q1r);
       }
-      if constexpr (CPT == 2) {
-        static_assert(sizeof(R) == 4, "two columns per thread: complex64 only");
-        *reinterpret_cast<float4*>(cp + (int64_t)i * N) = make_float4(re[0], im[0], re[1], im[1]);
-      } else {
-        cp[(int64_t)i * N] = C2{re[0], im[0]};
+    } else {
+      R yr[CPT][KMAX], yi[CPT][KMAX];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if constexpr (GATHER) {
+          const int64_t yo = gmap(tab, gm.Bb, b) + gmap(tab, gm.Bn, n + c);
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k) {
+            const C2 v = Yc[yo + kofs[1][k]];
+            yr[c][k] = v.x;
+            yi[c][k] = v.y;
+          }
+        } else if (K % V == 0) {
+#pragma unroll
+          for (int q = 0; q < KMAX / V; ++q) {
+            if (q * V < K) {
+              R vr[V], vi[V];
+              *reinterpret_cast<float4*>(vr) = __ldg(reinterpret_cast<const float4*>(yb + (n + c) * K) + q);
+              *reinterpret_cast<float4*>(vi) = __ldg(reinterpret_cast<const float4*>(yb + (N + n + c) * K) + q);
+#pragma unroll
+              for (int u = 0; u < V; ++u) { yr[c][q * V + u] = vr[u]; yi[c][q * V + u] = vi[u]; }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k)
+            if (k < K) { yr[c][k] = __ldg(yb + (n + c) * K + k); yi[c][k] = __ldg(yb + (N + n + c) * K + k); }
+        }
+      }
+      C2* __restrict__ cp = C + (b * M + m0) * N + n;
+      for (int i = rg; i < tm; i += groups) {
+        R re[CPT], im[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) { re[c] = 0; im[c] = 0; }
+        if (K % V == 0) {       // the row of X as 16-byte broadcast loads (the LDS count bounded this loop)
+#pragma unroll
+          for (int q = 0; q < KMAX / V; ++q) {
+            if (q * V < K) {
+              R xr[V], xi[V];
+              *reinterpret_cast<float4*>(xr) = *reinterpret_cast<const float4*>(&xs[0][i][q * V]);
+              *reinterpret_cast<float4*>(xi) = *reinterpret_cast<const float4*>(&xs[1][i][q * V]);
+#pragma unroll
+              for (int u = 0; u < V; ++u)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                  re[c] = fma(xr[u], yr[c][q * V + u], re[c]);
+                  re[c] = fma(-xi[u], yi[c][q * V + u], re[c]);
+                  im[c] = fma(xr[u], yi[c][q * V + u], im[c]);
+                  im[c] = fma(xi[u], yr[c][q * V + u], im[c]);
+                }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k) {
+            if (k < K) {
+              const R ar = xs[0][i][k], ai = xs[1][i][k];
+#pragma unroll
+              for (int c = 0; c < CPT; ++c) {
+                re[c] = fma(ar, yr[c][k], re[c]);
+                re[c] = fma(-ai, yi[c][k], re[c]);
+                im[c] = fma(ar, yi[c][k], im[c]);
+                im[c] = fma(ai, yr[c][k], im[c]);
+              }
+            }
+          }
+        }
+        if constexpr (CPT == 2) {
+          static_assert(sizeof(R) == 4, "two columns per thread: complex64 only");
+          *reinterpret_cast<float4*>(cp + (int64_t)i * N) = make_float4(re[0], im[0], re[1], im[1]);
+        } else {
+          cp[(int64_t)i * N] = C2{re[0], im[0]};
+        }
       }
     }
   }

@@ -454,6 +454,15 @@ Sk2Shape skinny2_shape(const TcStep& t) {
   return h;
 }
 
+// complex64 wide steps (gathered, K = 16) with packed fp32 pairs (FFMA2); TN_WIDE_FFMA2=0: scalar FFMA
+bool wide_ffma2() {
+  static const bool on = [] {
+    const char* e = std::getenv("TN_WIDE_FFMA2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // tensor maps of a staged skinny step's planar operands (in the arena at x_off / y_off)
 void set_skinny_maps(TcStep& t, char* base) {
   if (t.kind != K_SKINNY) return;
@@ -554,7 +563,14 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
           X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles, t.gmaps, tab_d);                     \
   }
       if constexpr (sizeof(R) == 4) {
-        if (two) { TN_WIDE(2, 0) TN_WIDE(2, 1) TN_WIDE(2, 2) TN_WIDE(2, 3) TN_WIDE(2, 4) }
+        // gathered, K = 16: the FFMA2 variant (8% faster there; no gain at K = 4, 8 -- bound
+        // by writing C; TN_WIDE_FFMA2=0: scalar FFMA)
+        if (two && t.gather && t.k_bits == 4 && wide_ffma2()) {
+          tnd::wide_kernel<R, 2, 16, true, true><<<grid, tnd::WD_THREADS, 0, st>>>(
+              X, Y, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, tiles, t.gmaps, tab_d);
+        } else if (two) {
+          TN_WIDE(2, 0) TN_WIDE(2, 1) TN_WIDE(2, 2) TN_WIDE(2, 3) TN_WIDE(2, 4)
+        }
       }
       if (!two) { TN_WIDE(1, 0) TN_WIDE(1, 1) TN_WIDE(1, 2) TN_WIDE(1, 3) TN_WIDE(1, 4) }
 #undef TN_WIDE

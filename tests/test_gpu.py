@@ -265,6 +265,7 @@ WIDE_CASES = [
     (0, 5, 6, 0, 2),          # K = 1 (outer product), ragged tiles (M = 32 rows, N = 64), permuted
     (3, 4, 8, 2, 6),          # batch 8, permuted
     (0, 10, 4, 4, 7),         # N = 16 < tile width
+    (2, 3, 12, 4, 3),         # batch 4, K = 16 (complex64: the FFMA2 variant), permuted
 ]
 
 
