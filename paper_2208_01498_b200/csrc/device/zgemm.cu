@@ -120,13 +120,21 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_kernel(const double* __
         br[j] = sBr[swz(n0, kk + t)];
         bi[j] = sBi[swz(n0, kk + t)];
       }
+      // the two products into one accumulator are 2 * 4 DMMAs apart (one pass per
+      // product term over every accumulator): back-to-back dependent DMMAs would stall
+      // each warp for the pipe's full latency
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
-          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
           dmma(ci[i][j], ar[i][0], ar[i][1], bi[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
           dmma(ci[i][j], ai[i][0], ai[i][1], br[j]);
         }
     }
@@ -168,13 +176,16 @@ __host__ __device__ constexpr int g_stage() { return (BM + BNT) * BK; }      // 
 template <int BNT>
 __host__ __device__ constexpr int g_smem() { return STAGES * g_stage<BNT>() * 16 + (BM + BNT) * 8 + 2 * G_KTAB * 8; }
 
+// ksplit in {2, 4} (the tail launch of a step whose tiles leave a partial last wave): the
+// ksplit CTAs of one tile form a cluster along y, each contracts a contiguous 1/ksplit of K,
+// and the leader (cluster rank 0) adds the others' accumulators from their shared memory
+// (DSMEM) in rank order -- deterministic, no zeroing pass, no atomics, no extra C traffic.
+// tile0: first linear tile (batch-major) of this launch; grid.x tiles, grid.y = ksplit.
 template <int BNT>
-// ksplit = 2: blockIdx.y takes one half of K and the halves are ADDED to a zeroed C by
-// fp64 atomics -- two addends onto 0.0 commute exactly, so the result is deterministic
-// (fills the partial last wave of a step with few tiles)
 __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const GatherMaps gm_, const int64_t* __restrict__ tab,
                                                                     void* const* __restrict__ ptrs, int32_t c_node,
-                                                                    int32_t M, int32_t N, int32_t K, int32_t ksplit) {
+                                                                    int32_t M, int32_t N, int32_t K, int32_t ksplit,
+                                                                    int64_t tile0) {
   constexpr int G_STAGE = g_stage<BNT>();
   constexpr int WN = BNT / 16, WM = 8 / WN;              // warp grid (N x M), warp tile 16 x (BM / WM)
   constexpr int MI = BM / WM / 16;                        // 16-row fragments per warp
@@ -190,13 +201,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
       kB[k] = gmap(tab, gm_.Bk, k);
     }
   const int n_tiles_m = (M + BM - 1) / BM, n_tiles_n = (N + BNT - 1) / BNT;
-  const int pid = blockIdx.x;
+  const int64_t lt = tile0 + blockIdx.x;                 // linear tile: batch-major
+  const int b = (int)(lt / (n_tiles_m * n_tiles_n));
+  const int pid = (int)(lt % (n_tiles_m * n_tiles_n));
   const int group = pid / (GROUP_M * n_tiles_n);
   const int first_m = group * GROUP_M;
   const int gmr = min(n_tiles_m - first_m, GROUP_M);
   const int m_blk = first_m + (pid % (GROUP_M * n_tiles_n)) % gmr;
   const int n_blk = (pid % (GROUP_M * n_tiles_n)) / gmr;
-  const int b = blockIdx.z;
   const double2* __restrict__ A = reinterpret_cast<const double2*>(ptrs[gm_.a_node]);
   const double2* __restrict__ B = reinterpret_cast<const double2*>(ptrs[gm_.b_node]);
   if (threadIdx.x < BM) {
@@ -274,16 +286,69 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
         br[j] = w.x;
         bi[j] = w.y;
       }
+      // the two products into one accumulator are MI * 4 DMMAs apart (one pass per
+      // product term over every accumulator): back-to-back dependent DMMAs would stall
+      // each warp for the pipe's full latency
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           dmma(cr[i][j], ar[i][0], ar[i][1], br[j]);
-          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
           dmma(ci[i][j], ar[i][0], ar[i][1], bi[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(cr[i][j], nai[i][0], nai[i][1], bi[j]);
           dmma(ci[i][j], ai[i][0], ai[i][1], br[j]);
         }
     }
+  }
+  if (ksplit > 1) {
+    // K-split cluster: the other ranks park their accumulators in their (now idle) stage
+    // buffers, the leader adds them in rank order over DSMEM
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    uint32_t crank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    double* red = reinterpret_cast<double*>(smz);           // [2 * MI * 2 * 4][THREADS]
+    static_assert(2 * MI * 2 * 4 * THREADS * 8 <= STAGES * G_STAGE * 16, "reduction buffer");
+    if (crank != 0) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            red[((i * 2 + j) * 8 + r) * THREADS + threadIdx.x] = cr[i][j][r];
+            red[((i * 2 + j) * 8 + 4 + r) * THREADS + threadIdx.x] = ci[i][j][r];
+          }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (crank == 0) {
+      for (int q = 1; q < ksplit; ++q) {
+        uint32_t base;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(base)
+                     : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(red + threadIdx.x))), "r"(q));
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              double vr, vi;
+              asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vr) : "r"(base + ((i * 2 + j) * 8 + r) * THREADS * 8));
+              asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vi) : "r"(base + ((i * 2 + j) * 8 + 4 + r) * THREADS * 8));
+              cr[i][j][r] += vr;
+              ci[i][j][r] += vi;
+            }
+      }
+    }
+    // no rank leaves (its shared memory) before the leader has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (crank != 0) return;
   }
   double2* C = reinterpret_cast<double2*>(ptrs[c_node]) + (int64_t)b * M * (int64_t)N;
 #pragma unroll
@@ -296,23 +361,10 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_dmma_gather_kernel(const Gat
         const int col = n_blk * BNT + wn + j * 8 + 2 * t;
         if (row < M && col < N) {
           double2* cp = C + (int64_t)row * N + col;
-          if (ksplit > 1) {
-            atomicAdd(&cp[0].x, cr[i][j][2 * h]);
-            atomicAdd(&cp[0].y, ci[i][j][2 * h]);
-            if (col + 1 < N) { atomicAdd(&cp[1].x, cr[i][j][2 * h + 1]); atomicAdd(&cp[1].y, ci[i][j][2 * h + 1]); }
-          } else {
-            cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
-            if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
-          }
+          cp[0] = double2{cr[i][j][2 * h], ci[i][j][2 * h]};
+          if (col + 1 < N) cp[1] = double2{cr[i][j][2 * h + 1], ci[i][j][2 * h + 1]};
         }
       }
-}
-
-// zero the complex128 node c_node (n elements): the split-K DMMA accumulates into it
-__global__ void zero_node_kernel(void* const* __restrict__ ptrs, int32_t c_node, int64_t n) {
-  double2* C = reinterpret_cast<double2*>(ptrs[c_node]);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    C[i] = double2{0.0, 0.0};
 }
 }  // namespace zg
 }  // namespace tnd

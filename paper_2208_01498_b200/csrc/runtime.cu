@@ -343,21 +343,47 @@ bool dmma_bn32(const TcStep&) {
   return v;
 }
 
-// split K in two for a gathered DMMA step whose 64 x 64 tiles leave most of a last wave idle
-// (2 CTAs per SM: 296 slots) and that keeps >= 8 K stages per half: an experiment switch
-// (TN_DMMA_KSPLIT=1), off by default -- measured slower on configs[3] (its DMMA 1.02 ->
-// 1.11 ms per amplitude: the zeroing pass, the fp64 atomics and the halved K per CTA cost
-// more than the 3.46-wave tail)
-int dmma_ksplit(const TcStep& t) {
+// Tail split of a gathered DMMA step (2 CTAs of 64 x 64 tiles per SM: 296 slots): T tiles
+// are F full waves plus r tiles.  The F waves run as one launch; the r tail tiles run as a
+// second launch with K split over clusters of ks in {2, 4} CTAs (the leader adds the
+// partial accumulators over DSMEM, zgemm.cu), so the tail takes ceil(ks r / 296) / ks of a
+// wave instead of one (configs[3]'s dominant step: 1024 tiles = 3 waves + 136 -> 3.5 wave
+// times).  ks is the choice with the least estimated time (+ 0.05 wave per split for the
+// reduction), each CTA keeping >= 128 of K.  An experiment switch (TN_DMMA_TAIL=1), off by
+// default: measured slower on configs[3] (its dominant step 0.577 -> 0.60 ms, DMMA 1.02 ->
+// 1.05 ms per amplitude): a partial wave of single CTAs per SM already runs near the SM's
+// DMMA rate (2 CTAs per SM share one pipe), and the second launch adds a drain bubble.
+struct DmmaSplit {
+  int64_t tiles = 0, n_main = 0;   // linear tiles (batch-major); the first n_main in the main launch
+  int ks = 1;                      // K split of the tail tiles (1: no tail launch)
+};
+DmmaSplit dmma_split(const TcStep& t) {
   static const bool on = [] {
-    const char* e = std::getenv("TN_DMMA_KSPLIT");
+    const char* e = std::getenv("TN_DMMA_TAIL");
     return e && e[0] == '1';
   }();
-  if (!on || !t.gather || dmma_bn32(t) || t.k_bits < 8) return 1;
-  const int64_t tiles = (((int64_t(1) << t.n_bits) + tnd::zg::BN - 1) / tnd::zg::BN) *
-                        (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM) << t.nb_bits;
-  const int64_t slots = 296, rem = tiles % slots;
-  return (tiles < 4 * slots && rem != 0 && rem < slots * 3 / 4) ? 2 : 1;
+  DmmaSplit d;
+  const int bn = dmma_bn32(t) ? 32 : tnd::zg::BN;
+  d.tiles = ((((int64_t(1) << t.n_bits) + bn - 1) / bn) * (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM))
+            << t.nb_bits;
+  d.n_main = d.tiles;
+  if (!on || !t.gather || dmma_bn32(t)) return d;
+  const int64_t S = 296, F = d.tiles / S, r = d.tiles % S;
+  if (r == 0) return d;
+  double best = (double)F + 1.0;
+  for (int ks : {2, 4}) {
+    if (t.k_bits - (ks == 2 ? 1 : 2) < 7) continue;
+    const double est = (double)F + (double)((ks * r + S - 1) / S) / ks + 0.05;
+    if (est < best) { best = est; d.ks = ks; }
+  }
+  if (d.ks > 1) d.n_main = F * S;
+  return d;
+}
+
+// kernel launches of a gathered DMMA step
+int dmma_launches(const TcStep& t) {
+  const DmmaSplit d = dmma_split(t);
+  return (d.n_main > 0 ? 1 : 0) + (d.ks > 1 ? 1 : 0);
 }
 
 void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st,
@@ -367,25 +393,39 @@ void launch_dmma(const TcStep& t, char* arena, void* const* ptrs_d, const int64_
   dim3 grid((unsigned)tiles, 1, 1u << t.nb_bits);
   if (t.gather) {
     if (mk) mk->mark(st, 2, TN_K_DMMA, profile_dump_ms() >= 0 ? shape_tag("dmma gather", t.nb_bits, t.m_bits, t.n_bits, t.k_bits) : "");
-    const int ks = dmma_ksplit(t);
-    if (ks > 1) {
-      const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
-      tnd::zg::zero_node_kernel<<<(unsigned)std::min<int64_t>((n_out + 255) / 256, 148 * 8), 256, 0, st>>>(
-          ptrs_d, t.c_node, n_out);
+    const DmmaSplit d = dmma_split(t);
+    const int32_t M = 1 << t.m_bits, N = 1 << t.n_bits, K = 1 << t.k_bits;
+    if (dmma_bn32(t)) {
+      ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<32>, tnd::zg::g_smem<32>());
+      tnd::zg::zgemm_dmma_gather_kernel<32><<<dim3((unsigned)d.tiles, 1, 1), tnd::zg::THREADS, tnd::zg::g_smem<32>(), st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, M, N, K, 1, int64_t(0));
+      g_launches++;
+      CK(cudaGetLastError());
+      return;
+    }
+    ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<64>, tnd::zg::g_smem<64>());
+    if (d.n_main > 0) {
+      tnd::zg::zgemm_dmma_gather_kernel<64><<<dim3((unsigned)d.n_main, 1, 1), tnd::zg::THREADS, tnd::zg::g_smem<64>(), st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, M, N, K, 1, int64_t(0));
       g_launches++;
     }
-    if (dmma_bn32(t)) {
-      const int64_t tiles32 = (((int64_t(1) << t.n_bits) + 31) / 32) * (((int64_t(1) << t.m_bits) + tnd::zg::BM - 1) / tnd::zg::BM);
-      ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<32>, tnd::zg::g_smem<32>());
-      tnd::zg::zgemm_dmma_gather_kernel<32><<<dim3((unsigned)tiles32, ks, 1u << t.nb_bits), tnd::zg::THREADS,
-                                              tnd::zg::g_smem<32>(), st>>>(
-          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, ks);
-    } else {
-      ensure_smem_attr((const void*)tnd::zg::zgemm_dmma_gather_kernel<64>, tnd::zg::g_smem<64>());
-      tnd::zg::zgemm_dmma_gather_kernel<64><<<dim3(grid.x, ks, grid.z), tnd::zg::THREADS, tnd::zg::g_smem<64>(), st>>>(
-          t.gmaps, tab_d, ptrs_d, t.c_node, 1 << t.m_bits, 1 << t.n_bits, 1 << t.k_bits, ks);
+    if (d.ks > 1) {              // the tail tiles, K split over clusters of d.ks CTAs
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(d.tiles - d.n_main), (unsigned)d.ks, 1);
+      cfg.blockDim = dim3(tnd::zg::THREADS, 1, 1);
+      cfg.dynamicSmemBytes = tnd::zg::g_smem<64>();
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1;
+      at[0].val.clusterDim.y = (unsigned)d.ks;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, tnd::zg::zgemm_dmma_gather_kernel<64>, t.gmaps, tab_d, ptrs_d, t.c_node, M, N, K,
+                            (int32_t)d.ks, d.n_main));
+      g_launches++;
     }
-    g_launches++;
     CK(cudaGetLastError());
     return;
   }
@@ -1105,7 +1145,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? (t.gather ? (dmma_ksplit(t) > 1 ? 2 : 1) : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
+        k += t.kind == K_DMMA ? (t.gather ? dmma_launches(t) : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }

@@ -316,9 +316,12 @@ def test_pair_skinny_k_slabs():
 DMMA_CASES = [
     (0, 6, 6, 4, None),       # one 64x64 tile, K = 16
     (0, 5, 7, 3, 2),          # ragged M = 32, N = 128, K = 8, permuted
-    (2, 7, 6, 9, 4),          # batch 4, K = 512 (32 stages), permuted
-    (0, 9, 9, 6, None),       # 64 tiles
-    (6, 10, 6, 9, 5),         # configs[3]'s dominant step: 1024 tiles = 3.46 waves -> K split in 2 (fp64 atomics)
+    (2, 7, 6, 9, 4),          # batch 4, K = 512 (32 stages), permuted (tail split: 8 tiles, K in 4)
+    (0, 9, 9, 6, None),       # 64 tiles, K too short to split
+    (6, 10, 6, 9, 5),         # configs[3]'s dominant step: 1024 tiles = 3 waves + 136 (tail split: K in 2)
+    (0, 9, 9, 10, None),      # 64 tiles, K = 1024 (tail split: one launch of clusters of 4)
+    (0, 5, 7, 8, 2),          # ragged M = 32, 2 tiles (tail split: K in 2)
+    (2, 9, 8, 8, 3),          # 128 tiles, K = 256, batch 4, permuted (tail split: K in 2)
 ]
 
 
@@ -330,25 +333,36 @@ def test_pair_complex128_dmma_path(case):
     assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
 
 
-def test_pair_complex128_dmma_ksplit():
-    """The K-split DMMA variant (TN_DMMA_KSPLIT=1, child process): configs[3]'s dominant
-    shape, 1024 tiles = 3.46 waves, K halves added by fp64 atomics onto a zeroed C --
-    within the DMMA bound and bit-identical over two runs (two addends onto 0 commute)."""
+def test_pair_complex128_dmma_tail_split():
+    """TN_DMMA_TAIL=1 (child process): the partial last wave of tiles runs as a second
+    launch with K split over clusters of 2 or 4 CTAs, the leader adding the partial
+    accumulators over DSMEM in rank order -- within the DMMA bound, bit-identical over two
+    runs, and within 1e-13 Σ|A||B| of the one-launch default (only the order of the K
+    summation differs)."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
         import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
-        ia, ib, ic, dims = T._gemm_case(6, 10, 6, 9, 5)
-        got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=7)
-        assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300)
-        again, _, _ = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=7)
-        assert np.array_equal(got, again)
+        for case in (2, 4, 5, 6, 7):
+            nb, m, n, k, ps = T.DMMA_CASES[case]
+            ia, ib, ic, dims = T._gemm_case(nb, m, n, k, ps)
+            got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
+            assert np.all(np.abs(got - ref) <= 1e-13 * bound + 1e-300), case
+            again, _, _ = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
+            assert np.array_equal(got, again), case
+            np.save(f'/tmp/dmma_tail_{case}.npy', got)
         print('ok')
     """)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                       env=dict(os.environ, TN_DMMA_KSPLIT="1"),
+                       env=dict(os.environ, TN_DMMA_TAIL="1"),
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    for case in (2, 4, 5, 6, 7):
+        nb, m, n, k, ps = DMMA_CASES[case]
+        ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+        got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_TC, seed=20 + case)
+        split = np.load(f'/tmp/dmma_tail_{case}.npy')
+        assert np.all(np.abs(got - split) <= 1e-13 * bound + 1e-300), case
 
 
 def test_pair_tensor_core_k_slabs(monkeypatch):
