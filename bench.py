@@ -330,10 +330,10 @@ def run_ours(args):
         os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line (no version banner)
     if distributed:
         import torch.distributed as tdist
-        # ranks on one host share its cores for the order search (tn_find_order threads)
-        lws = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-        os.environ.setdefault("TN_ORDER_THREADS", str(max(1, (os.cpu_count() or 1) // max(lws, 1))))
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # rank 0 alone runs the host order search (all cores) and broadcasts it
+        # (dist.shared_order); a long search must not trip the collective timeout
+        import datetime
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=datetime.timedelta(hours=2))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2208_01498_b200 as tb
@@ -344,7 +344,9 @@ def run_ours(args):
     c, bits = workload(ci)
     dtype = tb.TN_C64 if spec["dtype"] == "c64" else tb.TN_C128
     net = tb.Network.from_circuit(c, diag_hyper=spec["hyper"])
-    order = tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=spec["slice_log"])
+    order = pdist.shared_order(
+        lambda: tb.Order(net, seed=ORDER_SEED, n_seeds=spec["n_seeds"], max_log2_size=spec["slice_log"]),
+        lambda st, sl, mf: tb.Order.from_steps(net, st, sl, mf), device=dev)
     oinfo = order.info()
     plan = tb.Plan(net, order, dtype=dtype, device=local)      # raises if the arena does not fit
     pinfo = plan.info()

@@ -118,6 +118,20 @@ void tn_order_params_default(tn_order_params* p);
 int tn_find_order(tn_network net, const tn_order_params* params, uint64_t seed, tn_order* out);
 void tn_order_free(tn_order ord);
 
+/* tn_order_import: an order given explicitly -- the steps (host int32[2 * n_steps], the
+ * layout tn_order_steps returns) and sliced indices (host int32[n_slices], any order) of
+ * an order tn_find_order produced, e.g. on another rank (multi-GPU: one host order
+ * search per job, broadcast to the ranks; paper_2208_01498_b200/dist.py shared_order).
+ * The tree is SM Algorithm 1's output as a plain contraction sequence (PAPER.md l.80,
+ * Fig. 2: a binary tree over the network's tensors); the per-step Eq. (3) costs
+ * (l.82-86) are recomputed.  median_fallbacks is carried into tn_order_info as given.
+ * Errors: TN_EINVAL unless n_steps = n_tensors - 1 and every step contracts two distinct
+ * live nodes (leaves 0..n-1, step k creating node n + k), and the sliced indices are
+ * distinct closed (non-output) indices of `net`.  The caller keeps ownership of the
+ * arrays (copied); `net` must outlive the order. */
+int tn_order_import(tn_network net, const int32_t* steps, int32_t n_steps, const int32_t* slices,
+                    int32_t n_slices, int32_t median_fallbacks, tn_order* out);
+
 typedef struct {
   int32_t n_steps, n_slices;           /* n_slices = number of sliced indices */
   int32_t max_step_log2, max_size_log2; /* unsliced: max log2 M, max log2 result size */

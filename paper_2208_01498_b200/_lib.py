@@ -15,7 +15,7 @@ TN_PATH_AUTO, TN_PATH_SMALL, TN_PATH_TC, TN_PATH_SKINNY, TN_PATH_WIDE = 0, 1, 2,
 EXPORTED_SYMBOLS = [
     "tn_last_error", "tn_version", "tn_build_network", "tn_network_free", "tn_network_get_info",
     "tn_network_dims", "tn_network_tensor", "tn_order_params_default", "tn_find_order", "tn_order_free",
-    "tn_order_get_info", "tn_order_steps", "tn_order_slices", "tn_plan_create", "tn_plan_free",
+    "tn_order_get_info", "tn_order_steps", "tn_order_slices", "tn_order_import", "tn_plan_create", "tn_plan_free",
     "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_prepare", "tn_contract_prepared", "tn_amplitudes", "tn_contract_pair",
     "tn_kernel_launches",
 ]
@@ -80,6 +80,7 @@ def _load():
         "tn_order_params_default": (None, [C.POINTER(OrderParams)]),
         "tn_find_order": (C.c_int, [P, C.POINTER(OrderParams), C.c_uint64, C.POINTER(P)]),
         "tn_order_free": (None, [P]),
+        "tn_order_import": (C.c_int, [P, P, I32, P, I32, I32, C.POINTER(P)]),
         "tn_order_get_info": (C.c_int, [P, C.POINTER(_OrderInfo)]),
         "tn_order_steps": (C.c_int, [P, P]),
         "tn_order_slices": (C.c_int, [P, P]),
@@ -187,6 +188,21 @@ class Order:
         _check(lib.tn_find_order(net.h, C.byref(p), C.c_uint64(seed), C.byref(h)))
         self.h = h
         self.net = net          # the network must outlive the order
+
+    @classmethod
+    def from_steps(cls, net: Network, steps, slices=(), median_fallbacks=0):
+        """tn_order_import: an order given as its steps [(a, b), ...] and sliced indices
+        (e.g. found by another rank and broadcast, dist.shared_order)."""
+        st = np.ascontiguousarray(np.asarray(steps, np.int32).reshape(-1))
+        sl = np.ascontiguousarray(np.asarray(list(slices), np.int32))
+        st_p = _ptr(st) if st.size else None
+        sl_p = _ptr(sl) if sl.size else None
+        h = C.c_void_p()
+        _check(lib.tn_order_import(net.h, st_p, len(st) // 2, sl_p, len(sl), int(median_fallbacks), C.byref(h)))
+        o = cls.__new__(cls)
+        o.h = h
+        o.net = net
+        return o
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -645,4 +645,20 @@ Order find_order(const Network& net, uint64_t seed, const OrderParams& p) {
   return std::move(cand[best]);
 }
 
+// An order given as explicit steps and sliced indices (tn_order_import: the order another
+// rank found), validated by the caller as a full binary tree over the network's tensors;
+// the per-step costs are recomputed here (the same Eq. (3) counts find_order keeps).
+Order import_order(const Network& net, std::vector<std::pair<int, int>> steps, std::vector<int> slices,
+                   int median_fallbacks) {
+  Order o;
+  costs(net, steps, o.step_m, o.step_res);
+  double tot = 0.0;
+  for (int mm : o.step_m) tot = tot + std::ldexp(1.0, mm + 1);
+  o.total_2M = tot;
+  o.median_fallbacks = median_fallbacks;
+  o.steps = std::move(steps);
+  o.slices = std::move(slices);
+  return o;
+}
+
 }  // namespace tn

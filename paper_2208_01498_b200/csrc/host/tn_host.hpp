@@ -54,6 +54,9 @@ struct Order {
 
 // SM Algorithm 1 + Theorem 1 proof hierarchy + greedy leaves (R5-R10), slicing R11.
 Order find_order(const Network& net, uint64_t seed, const OrderParams& p);
+// explicit steps / sliced indices (already validated) with their Eq. (3) costs
+Order import_order(const Network& net, std::vector<std::pair<int, int>> steps, std::vector<int> slices,
+                   int median_fallbacks);
 std::vector<int> choose_slices(const Network& net, const std::vector<std::pair<int, int>>& steps,
                                int max_log2_size);
 

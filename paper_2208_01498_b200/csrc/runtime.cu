@@ -1917,6 +1917,46 @@ int tn_find_order(tn_network h, const tn_order_params* params, uint64_t seed, tn
     *out = o.release();
   });
 }
+int tn_order_import(tn_network h, const int32_t* steps, int32_t n_steps, const int32_t* slices, int32_t n_slices,
+                    int32_t median_fallbacks, tn_order* out) {
+  return guard([&] {
+    if (!h || !out || n_steps < 0 || n_slices < 0 || (n_steps > 0 && !steps) || (n_slices > 0 && !slices))
+      throw Err(TN_EINVAL, "tn_order_import: null or negative argument");
+    const tn::Network& net = h->net;
+    const int n = (int)net.tensors.size();
+    if (n_steps != std::max(n - 1, 0))
+      throw Err(TN_EINVAL, "tn_order_import: a contraction tree of " + std::to_string(n) + " tensors has " +
+                               std::to_string(std::max(n - 1, 0)) + " steps, got " + std::to_string(n_steps));
+    // every step takes two distinct live nodes (leaves 0..n-1 or earlier results) and
+    // creates node n + k: n - 1 such steps leave exactly one node, the root
+    std::vector<char> alive(n + n_steps, 0);
+    std::fill(alive.begin(), alive.begin() + n, 1);
+    std::vector<std::pair<int, int>> st(n_steps);
+    for (int k = 0; k < n_steps; ++k) {
+      const int a = steps[2 * k], b = steps[2 * k + 1];
+      if (a == b || a < 0 || b < 0 || a >= n + k || b >= n + k || !alive[a] || !alive[b])
+        throw Err(TN_EINVAL, "tn_order_import: step " + std::to_string(k) + " does not contract two live nodes");
+      alive[a] = alive[b] = 0;
+      alive[n + k] = 1;
+      st[k] = {a, b};
+    }
+    // sliced indices: distinct closed (non-output) indices of the network, kept sorted
+    std::vector<char> closed(net.dims.size(), 0);
+    for (int t = 0; t < n; ++t)
+      for (int i : net.closed_inds(t)) closed[i] = 1;
+    std::vector<int> sl(slices, slices + n_slices);
+    std::sort(sl.begin(), sl.end());
+    for (size_t j = 0; j < sl.size(); ++j)
+      if (sl[j] < 0 || sl[j] >= (int)closed.size() || !closed[sl[j]] || (j > 0 && sl[j] == sl[j - 1]))
+        throw Err(TN_EINVAL, "tn_order_import: sliced index " + std::to_string(sl[j]) +
+                                 " is not a distinct closed index of the network");
+    auto o = std::make_unique<tn_order_s>();
+    o->ord = tn::import_order(net, std::move(st), std::move(sl), median_fallbacks);
+    o->net = &net;
+    *out = o.release();
+  });
+}
+
 void tn_order_free(tn_order o) { delete o; }
 
 int tn_order_get_info(tn_order o, tn_order_info* info) {

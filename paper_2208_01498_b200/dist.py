@@ -10,7 +10,8 @@ on 8 GPUs is the code the tests run:
     slices per rank, the partial amplitudes summed with ONE all-reduce (NCCL over
     NVLink on the GPU path, gloo in the CPU tests).
 Every function takes the world size / rank explicitly or from the default process
-group; nothing here does contraction arithmetic.
+group; nothing here does contraction arithmetic.  shared_order: the host order search
+runs once per job (rank 0) and is broadcast.
 """
 from __future__ import annotations
 
@@ -52,6 +53,36 @@ def bitstring_steps(contributing_ids, rows, count: int):
         for s in contributing_ids(r, count - len(items)):
             items.append((r, s))
     return items
+
+
+def shared_order(find_order, import_order, device=None):
+    """One host order search per job: rank 0 runs find_order() (tn_find_order, with all
+    the host's cores), its steps, sliced indices and median-fallback count go to every
+    rank by two broadcasts of the default group, and the other ranks build the same
+    order with import_order(steps, slices, median_fallbacks) (tn_order_import).  Every
+    rank then holds the identical tree by construction (find_order is deterministic
+    anyway; this saves N - 1 searches that would share the host's cores).  find_order()
+    returns an object with steps(), slices() and info()["median_fallbacks"]."""
+    world, rank = world_rank()
+    if world == 1:
+        return find_order()
+    o = find_order() if rank == 0 else None
+    hdr = torch.zeros(3, dtype=torch.int64, device=device)
+    if rank == 0:
+        steps, slices = o.steps(), o.slices()
+        hdr[0], hdr[1], hdr[2] = len(steps), len(slices), int(o.info()["median_fallbacks"])
+    dist.broadcast(hdr, src=0)
+    n_st, n_sl, mf = (int(v) for v in hdr.cpu().tolist())
+    body = torch.zeros(max(2 * n_st + n_sl, 1), dtype=torch.int64, device=device)
+    if rank == 0:
+        flat = [v for ab in steps for v in ab] + list(slices)
+        if flat:
+            body[:len(flat)] = torch.tensor(flat, dtype=torch.int64)
+    dist.broadcast(body, src=0)
+    if rank == 0:
+        return o
+    v = body.cpu().tolist()
+    return import_order([(v[2 * k], v[2 * k + 1]) for k in range(n_st)], v[2 * n_st:2 * n_st + n_sl], mf)
 
 
 def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:

@@ -104,3 +104,46 @@ def test_slice_block_and_bitstring_steps():
     assert items == [(0, 0), (0, 2), (0, 4), (1, 1), (2, 0), (2, 1)]
     assert len(set(items)) == len(items)
     assert bitstring_steps(lambda r, n: contrib[r][:n], [1], 5) == [(1, 1)]
+
+
+def _order_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2208_01498_b200 as tb
+    from paper_2208_01498_b200.dist import shared_order
+    from tn_inputs import sycamore
+    from oracle.network import build_network
+    from oracle.ssa import find_order, choose_slices
+    c = sycamore(4, 3, 4, 5)
+    net = tb.Network.from_circuit(c)
+    calls = []
+
+    def find():
+        calls.append(rank)
+        return tb.Order(net, seed=3, n_seeds=2, max_log2_size=4)
+
+    o = shared_order(find, lambda st, sl, mf: tb.Order.from_steps(net, st, sl, mf))
+    on = build_network(c)
+    steps, _ = find_order(on, seed=3, n_seeds=2, max_log2_size=4)
+    q.put((rank, calls, o.steps(), o.slices(), o.info(), steps, choose_slices(on, steps, 4)))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gloo_shared_order():
+    """dist.shared_order (bench.py under torchrun): rank 0 alone runs the order search,
+    rank 1 imports the broadcast steps and sliced indices (tn_order_import) -- both hold
+    the oracle's order and slices, with the same order info."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_order_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=600) for _ in range(2)], key=lambda g: g[0])
+    for p in procs:
+        p.join(timeout=60)
+    (r0, calls0, st0, sl0, inf0, osteps, oslices), (r1, calls1, st1, sl1, inf1, _, _) = got
+    assert calls0 == [0] and calls1 == []
+    assert st0 == st1 == osteps and sl0 == sl1 == oslices and len(sl0) >= 1
+    assert inf0 == inf1

@@ -1,7 +1,7 @@
 """The multi-rank path that bench.py runs, with 2 ranks on cuda:0 (-m gpu): slices of one
 amplitude partitioned by dist.slice_block and summed by dist.allreduce_sum_ on CUDA
 tensors (gloo backend: one GPU is reachable, the ranks never wait on each other's
-kernels), bitstrings partitioned by dist.block_range / dist.bitstring_steps; the
+kernels), the order found by rank 0 and imported by rank 1 (dist.shared_order), bitstrings partitioned by dist.block_range / dist.bitstring_steps; the
 reduced results against the oracle."""
 import os
 import socket
@@ -39,7 +39,9 @@ def _worker(rank, world, port, q):
     # plan (3 sliced bits) and a complex128 lattice plan (4 sliced bits)
     for name, circ, dtype, tgt in (("syc", sycamore(6, 3), tb.TN_C64, 16), ("lat", lattice_cz(5, 5, 10, 2), tb.TN_C128, 12)):
         net = tb.Network.from_circuit(circ)
-        order = tb.Order(net, seed=0, max_log2_size=tgt)
+        # the order as bench.py gets it: rank 0 searches, rank 1 imports the broadcast
+        order = pdist.shared_order(lambda: tb.Order(net, seed=0, max_log2_size=tgt),
+                                   lambda st, sl, mf: tb.Order.from_steps(net, st, sl, mf), device=dev)
         plan = tb.Plan(net, order, dtype=dtype, device=0)
         x = random_bitstrings(circ.n, 1, 4)[0]
         n_sl = plan.info()["n_slices"]

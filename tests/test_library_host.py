@@ -121,3 +121,31 @@ def test_bench_orders_bit_identical_to_oracle_files(ci):
     assert co.steps() == [tuple(p) for p in o["steps"]]
     assert co.slices() == o["slices"]
     assert co.info()["median_fallbacks"] == o["median_fallbacks"]
+
+
+def test_order_import_roundtrip_and_validation():
+    """tn_order_import: an order rebuilt from its steps and sliced indices has the same
+    steps, slices and info (Eq. (3) costs recomputed); malformed trees and sliced
+    indices are refused with TN_EINVAL (the handle is not created)."""
+    c = lattice_cz(4, 4, 8, 2)
+    net = tb.Network.from_circuit(c)
+    o = tb.Order(net, seed=5, n_seeds=2, max_log2_size=6)
+    st, sl = o.steps(), o.slices()
+    assert len(sl) >= 1
+    o2 = tb.Order.from_steps(net, st, list(reversed(sl)), o.info()["median_fallbacks"])
+    assert o2.steps() == st and o2.slices() == sl and o2.info() == o.info()
+    n = net.info()["n_tensors"]
+    d, out = net.dims()
+    bad_steps = [
+        st[:-1],                                    # one step short: no single root
+        [(st[0][0], st[0][0])] + st[1:],            # a node contracted with itself
+        [(st[0][0], n + 5)] + st[1:],               # a node not yet created
+        st[:1] + [(st[0][0], st[1][1])] + st[2:],   # a consumed node reused
+        [(-1, st[0][1])] + st[1:],
+    ]
+    for bs in bad_steps:
+        with pytest.raises(tb.TnError, match="tn_order_import"):
+            tb.Order.from_steps(net, bs, sl)
+    for bsl in ([sl[0], sl[0]], [len(d)], [-1], [int(out[0])]):
+        with pytest.raises(tb.TnError, match="tn_order_import"):
+            tb.Order.from_steps(net, st, bsl)
