@@ -664,4 +664,156 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
   }
 }
 
+// C[b][o] (+)= sum_s partial[b][s][o] for few outputs (n_out <= 4 x 148): one CTA per
+// output, thread t sums s = t, t + 256, ... in order, then a fixed tree over the CTA
+// (deterministic) -- the warp-per-output kernel above leaves a scalar's S partials to one
+// warp (configs[3]'s K = 2^20 dot product: 29 us)
+template <typename R>
+__global__ void __launch_bounds__(256) skinny_reduce_cta_kernel(const double2* __restrict__ partial, int32_t S,
+                                                                int32_t O, int64_t n_out, void* const* __restrict__ ptrs,
+                                                                int32_t c_node, int32_t accumulate) {
+  using C2 = typename cplx_t<R>::type;
+  __shared__ double2 red[256];
+  C2* C = reinterpret_cast<C2*>(ptrs[c_node]);
+  for (int64_t i = blockIdx.x; i < n_out; i += gridDim.x) {
+    const int64_t b = i / O, o = i % O;
+    double re = 0.0, im = 0.0;
+    for (int s = threadIdx.x; s < S; s += 256) {
+      const double2 v = partial[(b * S + s) * O + o];
+      re += v.x;
+      im += v.y;
+    }
+    red[threadIdx.x] = double2{re, im};
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (threadIdx.x < h) {
+        red[threadIdx.x].x += red[threadIdx.x + h].x;
+        red[threadIdx.x].y += red[threadIdx.x + h].y;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      double r = red[0].x, m = red[0].y;
+      if (accumulate) { r += C[i].x; m += C[i].y; }
+      C[i] = C2{(R)r, (R)m};
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------- batched skinny, gathered ----
+// Skinny steps without K-slabs (Eq. (3): C[b][m][n] =
+// sum_k X[b][m][k] Y[b][n][k], M N <= 256): one CTA per batch (grid-stride) stages chunks of
+// KC of K of X[b] and Y[b] in shared memory, gathering the raw interleaved operands
+// through the step's offset tables (GatherMaps: no planar pack pass, no K split, no
+// reduction launch), k-major ([k][row]) so the output threads read conflict-free.  The 256
+// threads are M N outputs x G = 256 / (M N) lanes of K (lane j takes k = j, j + G, ...); the
+// lanes' fp64 sums are added in lane order (deterministic).  Products and sums in fp64
+// for both dtypes.
+constexpr int BS_THREADS = 256;
+template <typename C2>
+__device__ __forceinline__ void bs_cp_async(C2* smem, const C2* gmem) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(C2) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem) : "memory");
+}
+template <typename R>
+__global__ void __launch_bounds__(BS_THREADS) bskinny_kernel(const GatherMaps gm, const int64_t* __restrict__ tab,
+                                                              void* const* __restrict__ ptrs, int32_t c_node,
+                                                              int32_t m_bits, int32_t n_bits, int32_t k_bits,
+                                                              int32_t kc_bits, int64_t n_batches, int32_t s_bits,
+                                                              double2* __restrict__ partial) {
+  using C2 = typename cplx_t<R>::type;
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  const int M = 1 << m_bits, N = 1 << n_bits, KC = 1 << kc_bits;
+  const int64_t K = int64_t(1) << k_bits;
+  const int MP = M + 1, NP = N + 1;                           // padded rows: conflict-free staging
+  C2* xs = reinterpret_cast<C2*>(bs_smem);                    // [KC][M + 1]
+  C2* ys = xs + KC * MP;                                      // [KC][N + 1]
+  int64_t* rowX = reinterpret_cast<int64_t*>(ys + KC * NP);   // [M]
+  int64_t* rowY = rowX + M;                                   // [N]
+  int64_t* kX = rowY + N;                                     // [KC]
+  int64_t* kY = kX + KC;                                      // [KC]
+  double2* red = reinterpret_cast<double2*>(kY + KC);         // [BS_THREADS]
+  const C2* __restrict__ A = reinterpret_cast<const C2*>(ptrs[gm.a_node]);
+  const C2* __restrict__ B = reinterpret_cast<const C2*>(ptrs[gm.b_node]);
+  C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
+  const int O = M * N, G = BS_THREADS / O;                    // O <= 256: G >= 1
+  const int o = threadIdx.x / G, j = threadIdx.x % G;
+  const int om = o / N, on = o % N;
+  // items (batch, K range): 2^s_bits contiguous K ranges per batch (few batches, long K);
+  // with more than one range the CTA writes partial[b][range][o] (summed in order by
+  // skinny_reduce_*_kernel) instead of C
+  const int64_t KR = K >> s_bits;
+  for (int64_t item = blockIdx.x; item < (n_batches << s_bits); item += gridDim.x) {
+    const int64_t b = item >> s_bits, kr = item & ((int64_t(1) << s_bits) - 1);
+    __syncthreads();                                          // the previous item's reads are done
+    for (int r = threadIdx.x; r < M + N; r += BS_THREADS) {
+      if (r < M) rowX[r] = gmap(tab, gm.Ab, b) + gmap(tab, gm.Am, r);
+      else rowY[r - M] = gmap(tab, gm.Bb, b) + gmap(tab, gm.Bn, r - M);
+    }
+    double re = 0.0, im = 0.0;
+    for (int64_t k0 = kr * KR; k0 < (kr + 1) * KR; k0 += KC) {
+      __syncthreads();                                        // rows ready / previous chunk consumed
+      for (int k = threadIdx.x; k < KC; k += BS_THREADS) {
+        kX[k] = gmap(tab, gm.Ak, k0 + k);
+        kY[k] = gmap(tab, gm.Bk, k0 + k);
+      }
+      __syncthreads();
+      // gather along the operand's stride-1 direction (K or rows) so a warp's loads
+      // coalesce; cp.async straight to shared memory (every element's load in flight at once)
+      for (int e = threadIdx.x; e < M * KC; e += BS_THREADS) {
+        const int r = gm.a_kfast ? e >> kc_bits : e & (M - 1);
+        const int k = gm.a_kfast ? e & (KC - 1) : e >> m_bits;
+        bs_cp_async(&xs[k * MP + r], &A[rowX[r] + kX[k]]);
+      }
+      for (int e = threadIdx.x; e < N * KC; e += BS_THREADS) {
+        const int r = gm.b_kfast ? e >> kc_bits : e & (N - 1);
+        const int k = gm.b_kfast ? e & (KC - 1) : e >> n_bits;
+        bs_cp_async(&ys[k * NP + r], &B[rowY[r] + kY[k]]);
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+      // four independent accumulator pairs (k = j + G (4 i + u)) hide the FMA latency
+      double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
+      int k = j;
+      for (; k + 3 * G < KC; k += 4 * G) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const C2 x = xs[(k + u * G) * MP + om], y = ys[(k + u * G) * NP + on];
+          const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+          ar[u] = fma(xr, yr, fma(-xi, yi, ar[u]));
+          ai[u] = fma(xr, yi, fma(xi, yr, ai[u]));
+        }
+      }
+      for (; k < KC; k += G) {
+        const C2 x = xs[k * MP + om], y = ys[k * NP + on];
+        const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+        ar[0] = fma(xr, yr, fma(-xi, yi, ar[0]));
+        ai[0] = fma(xr, yi, fma(xi, yr, ai[0]));
+      }
+      re += (ar[0] + ar[1]) + (ar[2] + ar[3]);
+      im += (ai[0] + ai[1]) + (ai[2] + ai[3]);
+    }
+    red[threadIdx.x] = double2{re, im};
+    __syncthreads();
+    if (threadIdx.x < O) {
+      double sr = 0.0, si = 0.0;
+      for (int q = 0; q < G; ++q) {
+        sr += red[threadIdx.x * G + q].x;
+        si += red[threadIdx.x * G + q].y;
+      }
+      const int mm = threadIdx.x / N, nn = threadIdx.x % N;
+      if (s_bits > 0) partial[(item << (m_bits + n_bits)) + threadIdx.x] = double2{sr, si};
+      else C[(b * M + mm) * (int64_t)N + nn] = C2{(R)sr, (R)si};
+    }
+  }
+}
+__host__ __device__ constexpr int bskinny_smem(int m_bits, int n_bits, int kc_bits, int esz) {
+  return (((1 << m_bits) + (1 << n_bits) + 2) << kc_bits) * esz + ((1 << m_bits) + (1 << n_bits)) * 8 +
+         2 * (1 << kc_bits) * 8 + BS_THREADS * 16;
+}
+
 }  // namespace tnd

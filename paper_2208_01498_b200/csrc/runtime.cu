@@ -503,9 +503,35 @@ bool wide_ffma2() {
   return on;
 }
 
+// skinny steps without K-slabs (K <= 2^22) read their raw operands (bskinny_kernel,
+// skinny.cu): one CTA per (batch, K range), no planar packs; a reduction launch only when
+// few batches split K.  configs[3]'s (10, 4, 4, 7) step: packs + staged kernel 101 us ->
+// 45 us; TN_SKINNY_GATHER=0 packs instead
+bool bskinny_ok(const TcStep& t) {
+  static const bool on = [] {
+    const char* e = std::getenv("TN_SKINNY_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return on && t.kind == K_SKINNY && t.n_slabs == 1 && t.k_bits <= 22 && t.m_bits + t.n_bits <= 8;
+}
+// K ranges per batch of a gathered skinny step: enough items for 4 CTAs per SM, each range
+// >= 256 of K
+int bskinny_s_bits(const TcStep& t) {
+  int s = 0;
+  while ((int64_t(1) << (t.nb_bits + s)) < 4 * 148 && t.k_bits - s > 8) ++s;
+  return s;
+}
+// K chunk staged per item: the largest with <= 48 KB of shared memory (4 CTAs per SM)
+int bskinny_s_bits(const TcStep& t);
+int bskinny_kc_bits(const TcStep& t) {
+  int kc = t.k_bits - bskinny_s_bits(t);             // a chunk never crosses a K range
+  while (kc > 0 && tnd::bskinny_smem(t.m_bits, t.n_bits, kc, t.esz) > 48 * 1024) --kc;
+  return kc;
+}
+
 // tensor maps of a staged skinny step's planar operands (in the arena at x_off / y_off)
 void set_skinny_maps(TcStep& t, char* base) {
-  if (t.kind != K_SKINNY) return;
+  if (t.kind != K_SKINNY || t.gather) return;
   const Sk2Shape h = skinny2_shape(t);
   if (!h.use) return;
   t.ta = make_planar_map(base + t.x_off, t.k_lo, t.m_bits, t.nb_bits, h.ks, (1 << t.m_bits) / h.m_split, t.esz / 2);
@@ -543,6 +569,29 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
     if (mk) mk->mark(st, 0, t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE,
                      dump ? shape_tag(t.kind == K_SKINNY ? "skinny" : "wide", t.nb_bits, t.m_bits, t.n_bits,
                                              t.k_bits) : "");
+    if (t.kind == K_SKINNY && t.gather) {     // batched skinny, gathered: one CTA per batch
+      const int kcb = bskinny_kc_bits(t);
+      const int smem = tnd::bskinny_smem(t.m_bits, t.n_bits, kcb, t.esz);
+      ensure_smem_attr((const void*)tnd::bskinny_kernel<R>, 48 * 1024 + 4096);
+      const int64_t nbat = int64_t(1) << t.nb_bits;
+      const int sb = bskinny_s_bits(t);
+      double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
+      tnd::bskinny_kernel<R><<<(unsigned)std::min<int64_t>(nbat << sb, 148 * 4), tnd::BS_THREADS, smem, st>>>(
+          t.gmaps, tab_d, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, kcb, nbat, sb, partial);
+      g_launches++;
+      if (sb > 0) {
+        if (mk) mk->mark(st, 3, TN_K_REDUCE);
+        const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
+        if (n_out <= 4 * 148)
+          tnd::skinny_reduce_cta_kernel<R><<<(unsigned)n_out, 256, 0, st>>>(
+              partial, 1 << sb, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, 0);
+        else
+          tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
+              partial, 1 << sb, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, 0);
+        g_launches++;
+      }
+      continue;
+    }
     const Sk2Shape h2 = t.kind == K_SKINNY ? skinny2_shape(t) : Sk2Shape{};
     if (t.kind == K_SKINNY && h2.use) {
       const int64_t K = int64_t(1) << t.k_lo;
@@ -562,8 +611,12 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       if (t.S * h2.wpg == 1) continue;   // the kernel wrote C
       if (mk) mk->mark(st, 3, TN_K_REDUCE);
       const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
-      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
-          partial, t.S * h2.wpg, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      if (n_out <= 4 * 148)
+        tnd::skinny_reduce_cta_kernel<R><<<(unsigned)n_out, 256, 0, st>>>(
+            partial, t.S * h2.wpg, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      else
+        tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
+            partial, t.S * h2.wpg, 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
       g_launches++;
     } else if (t.kind == K_SKINNY) {
       const int64_t K = int64_t(1) << t.k_lo;
@@ -584,8 +637,12 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       if (t.S * ws == 1) continue;      // the kernel wrote C
       if (mk) mk->mark(st, 3, TN_K_REDUCE);
       const int64_t n_out = int64_t(1) << (t.nb_bits + t.m_bits + t.n_bits);
-      tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
-          partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      if (n_out <= 4 * 148)
+        tnd::skinny_reduce_cta_kernel<R><<<(unsigned)n_out, 256, 0, st>>>(
+            partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
+      else
+        tnd::skinny_reduce_kernel<R><<<(unsigned)std::min<int64_t>((n_out + 7) / 8, 148 * 16), 256, 0, st>>>(
+            partial, t.S * skinny_ws(t), 1 << (t.m_bits + t.n_bits), n_out, ptrs_d, t.c_node, s > 0);
       g_launches++;
     } else {
       // complex64 with N >= 2: two adjacent columns per thread
@@ -792,7 +849,9 @@ void finish_tc_shape(TcStep& t) {
   }
 }
 int64_t tc_partial_bytes(const TcStep& t) {
-  if (t.kind == K_SKINNY) return (int64_t(16) * t.S * skinny_ws(t)) << (t.nb_bits + t.m_bits + t.n_bits);
+  if (t.kind == K_SKINNY)
+    return t.gather ? (bskinny_s_bits(t) > 0 ? int64_t(16) << (t.nb_bits + bskinny_s_bits(t) + t.m_bits + t.n_bits) : 0)
+                    : (int64_t(16) * t.S * skinny_ws(t)) << (t.nb_bits + t.m_bits + t.n_bits);
   if (t.kind != K_TC) return 0;
   return t.S > 1 ? (int64_t(8) * t.S) << (t.nb_bits + t.m_bits + t.n_bits) : 0;
 }
@@ -943,7 +1002,7 @@ std::vector<int> slab_k_order(const std::vector<int>& contr, const NodeLayout& b
 void set_gather_maps(TcStep& t, TabPool& pool, int X, const NodeLayout& LX, int Y, const NodeLayout& LY,
                      const std::vector<int>& batch, const std::vector<int>& fx, const std::vector<int>& fy,
                      const std::vector<int>& kord, const std::vector<int>& l2) {
-  if (t.kind == K_DMMA ? !dmma_gather_enabled() : t.kind == K_WIDE ? !wide_gather_enabled() : true) return;
+  if (t.kind == K_DMMA ? !dmma_gather_enabled() : t.kind == K_WIDE ? !wide_gather_enabled() : !bskinny_ok(t)) return;
   t.gather = true;
   auto& g = t.gmaps;
   g.Ab = pool.add(group_of(batch, LX, l2));
@@ -1145,7 +1204,7 @@ struct tn_plan_s {
       } else {
         launch_tc(tcs_l[L.second], arena_l, ptrs_l, tab_d, st);
         const auto& t = tcs_l[L.second];
-        k += t.kind == K_DMMA ? (t.gather ? dmma_launches(t) : 3) : t.kind == K_SKINNY ? (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
+        k += t.kind == K_DMMA ? (t.gather ? dmma_launches(t) : 3) : t.kind == K_SKINNY ? (t.gather ? (bskinny_s_bits(t) > 0 ? 2 : 1) : (t.S * skinny_ws(t) == 1 ? 3 : 4) * t.n_slabs) : t.kind == K_WIDE ? (t.gather ? 1 : 3) * t.n_slabs
              : t.n_mslabs * t.n_slabs * (t.S > 1 ? 3 : 2) + (t.n_mslabs > 1 ? 1 : t.n_slabs);
       }
     }

@@ -258,7 +258,11 @@ SKINNY_CASES = [
     (0, 4, 4, 12, 9),         # M = N = 16: 16 groups -> items on halves of X's rows, permuted
     (3, 1, 2, 10, 1),         # batch 8, one 2 x 4 group: 8 warps share its stage iterations
     (0, 0, 0, 20, None),      # configs[3]'s scalar K = 2^20 step: 16 warps take one group's stages in turn
-    (10, 4, 4, 7, 2),         # configs[3]'s batched skinny step
+    (10, 4, 4, 7, 2),         # configs[3]'s batched skinny step (gathered: one CTA per batch)
+    (6, 0, 0, 10, 3),         # gathered: 64 scalar dot products, 256 lanes of K per output
+    (7, 6, 2, 8, 4),          # gathered: M = 64, N = 4, K staged in 4 chunks
+    (8, 3, 3, 6, None),       # gathered: 64 outputs x 4 lanes, 256 batches
+    (9, 2, 5, 9, 5),          # gathered: 128 outputs x 2 lanes, K = 512 in chunks, permuted
 ]
 WIDE_CASES = [
     (0, 7, 9, 3, None),       # 128 x 512 outputs, K = 8
@@ -290,6 +294,38 @@ def test_pair_wide_path(case, dtype):
     # complex64 accumulates in fp32 (K <= 16): the fp32-path bound
     tol = 1e-12 if dtype == tb.TN_C128 else c64_tol(2 ** k)
     assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
+
+
+def test_pair_skinny_gather_off():
+    """TN_SKINNY_GATHER=0 (child process): every skinny case through planar packs + the
+    staged (TMA) or v1 split-K kernel + the ordered reduction instead of the gathering
+    kernel (one CTA per batch and K range) -- within the bound in both dtypes, and the
+    two complex128 results within 1e-12 of each other."""
+    import subprocess, sys, textwrap
+    cases = list(range(len(SKINNY_CASES)))
+    code = textwrap.dedent(f"""
+        import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+        import numpy as np, test_gpu as T, paper_2208_01498_b200 as tb
+        for case in {cases}:
+            nb, m, n, k, ps = T.SKINNY_CASES[case]
+            ia, ib, ic, dims = T._gemm_case(nb, m, n, k, ps)
+            got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C64, tb.TN_PATH_SKINNY, seed=50 + case)
+            assert np.all(np.abs(got - ref) <= T.c64_tol(8) * bound + 1e-30), case
+            got, ref, bound = T._run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_SKINNY, seed=50 + case)
+            assert np.all(np.abs(got - ref) <= 1e-12 * bound + 1e-30), case
+            np.save(f'/tmp/skinny_nogather_{{case}}.npy', got)
+        print('ok')
+    """)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env=dict(os.environ, TN_SKINNY_GATHER="0"),
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    for case in cases:
+        nb, m, n, k, ps = SKINNY_CASES[case]
+        ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+        got, ref, bound = _run_pair(ia, ib, ic, dims, tb.TN_C128, tb.TN_PATH_SKINNY, seed=50 + case)
+        other = np.load(f'/tmp/skinny_nogather_{case}.npy')
+        assert np.all(np.abs(got - other) <= 1e-12 * bound + 1e-30), case
 
 
 def test_pair_skinny_k_slabs():
