@@ -490,7 +490,14 @@ __device__ __forceinline__ void fma2_(uint64_t& d, uint64_t a, uint64_t b) {
 // ran at the FP64 pipe's ~12 TFLOP/s, 4x slower than writing C), fp64 for complex128.
 // KMAX = K (a template argument): the Y row lives in K-sized register arrays, so short-K
 // steps keep the occupancy (the 16-wide arrays held 128 registers at any K).
+#ifndef TN_WD_TM_C128
+#define TN_WD_TM_C128 64
+#endif
 constexpr int WD_THREADS = 256, WD_TM = 32, WD_MAXK = 16;
+// rows per tile: 32 for complex64, 64 for complex128 (fewer tiles per batch: configs[3]'s
+// (11, 7, 7, 2) step re-read Y once per 32-row tile)
+template <typename R>
+__host__ __device__ constexpr int wd_tm() { return sizeof(R) == 8 ? TN_WD_TM_C128 : WD_TM; }
 
 // GATHER: X and Y are the raw operands (interleaved complex, any stored index order), read
 // through the step's offset tables `gm` (no planar pack pass; the tables' K offsets go to
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
   // CPT adjacent columns per thread (2 for complex64: each broadcast X load serves two
   // outputs and each thread stores 16 bytes)
   using C2 = typename cplx_t<R>::type;
-  __shared__ __align__(16) R xs[2][WD_TM][WD_MAXK];  // (rows of KMAX <= WD_MAXK)
+  __shared__ __align__(16) R xs[2][wd_tm<R>()][WD_MAXK];  // (rows of KMAX <= WD_MAXK)
   __shared__ int64_t kofs[2][KMAX];                  // GATHER: K offsets of X and Y
   C2* __restrict__ C = reinterpret_cast<C2*>(ptrs[c_node]);
   const int64_t M = int64_t(1) << m_bits, N = int64_t(1) << n_bits;
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(WD_THREADS) wide_kernel(const R* __restrict__ 
       kofs[1][threadIdx.x] = gmap(tab, gm.Bk, threadIdx.x);
     }
   }
-  const int tm = (int)(M < WD_TM ? M : WD_TM);
+  const int tm = (int)(M < wd_tm<R>() ? M : wd_tm<R>());
   constexpr int TN = WD_THREADS * CPT;
   const int64_t mt = M / tm, ncb = (N + TN - 1) / TN;
   // N < TN: the threads split into row groups, each covering all N columns

@@ -647,7 +647,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
     } else {
       // complex64 with N >= 2: two adjacent columns per thread
       const bool two = sizeof(R) == 4 && t.n_bits >= 1;
-      const int64_t tm = std::min(tnd::WD_TM, 1 << t.m_bits), tn = int64_t(tnd::WD_THREADS) * (two ? 2 : 1);
+      const int64_t tm = std::min(tnd::wd_tm<R>(), 1 << t.m_bits), tn = int64_t(tnd::WD_THREADS) * (two ? 2 : 1);
       const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits)) / tm * (((int64_t(1) << t.n_bits) + tn - 1) / tn);
       const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
 #define TN_WIDE(CPT, KB)                                                                                    \
