@@ -194,9 +194,12 @@ int tn_contract(tn_plan plan, const uint8_t* bits, int64_t slice_begin, int64_t 
  * the intermediates still contribute exactly as computed. */
 int tn_contract_device(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin,
                        int64_t slice_end, void* amp_dev, void* stream);
-/* tn_contract_profiled: as tn_contract_device, but launches eagerly (no graph) with
- * CUDA events around every launch on `stream`; prof (host) receives the summed
- * device time per kernel class and the algorithmic flops of the GEMM launches. */
+/* tn_contract_profiled: as tn_contract_device, but with CUDA events around every kernel
+ * class on `stream`: it replays a profiled CUDA graph of the prologue / a slice (the
+ * plan's launches with event records between them, captured on first use; eager
+ * launches with TN_PROFILE_GRAPH=0) and synchronizes `stream`; prof (host) receives the
+ * summed device time per kernel class and the algorithmic flops / bytes.  The same holds
+ * for tn_prepare / tn_contract_prepared with a profile. */
 /* kernel classes of tn_profile.k_*: small-path waves, fp16x2 tensor-core pack, the
  * complex64 tcgen05 GEMMs (single-CTA cgemm_f16x2s_kernel, one-tile-per-pair
  * cgemm2_f16x2s_kernel, persistent pair cgemm2p_f16x2s_kernel), planar pack (skinny /

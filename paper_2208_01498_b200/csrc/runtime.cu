@@ -285,7 +285,12 @@ struct Marks {
   void mark(cudaStream_t st, int cat, int k, std::string tag = "") {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(e, st));
+    // under stream capture (a profiled graph) the record must become an external event
+    // record node: a plain record is only an intra-graph dependency marker, not timed
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK(cudaEventRecord(e, st));
     v.push_back({e, cat});
     fine.push_back(k);
     tags.push_back(std::move(tag));
@@ -1132,6 +1137,22 @@ struct tn_plan_s {
   int64_t frontier_bytes = 0;
   int64_t kernels_pro = 0;
   cudaGraphExec_t graph_pro = nullptr;
+  // profiled graphs of the prologue / a slice (profile_phase), captured on first use
+  struct ProfGraph {
+    cudaGraphExec_t exec = nullptr;
+    Marks mk;
+    tn_profile stat{};
+    int64_t kernels = 0;
+    bool failed = false;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      for (auto& e : mk.v) cudaEventDestroy(e.first);
+      mk = Marks();
+      stat = tn_profile{};
+    }
+  };
+  ProfGraph prof_graph[2];
   bool prepared = false;            // tn_prepare ran and no other contraction call since
   int64_t n_slices = 1;
   int slice_bits = 0;
@@ -1243,6 +1264,7 @@ struct tn_plan_s {
     }
     if (graph) cudaGraphExecDestroy(graph);
     if (graph_pro) cudaGraphExecDestroy(graph_pro);
+    for (auto& g : prof_graph) g.reset();
     if (cap) cudaStreamDestroy(cap);
     for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
     for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
@@ -1725,96 +1747,162 @@ void add_lane(tn_plan_s& P) {
   P.extra.push_back(std::move(l));
 }
 
-// one eager pass of a phase (0: prologue, 1: the slice at *slice_d) with CUDA events
-// around every kernel class; the device times and algorithmic flops / bytes are ADDED to pr
-void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
-  {
-    Marks mk;
-    mk.mark(st, 4, TN_K_OTHER);
-    tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
-        P.ptrs_d, P.leaf_base_d, P.var_begin_d, P.var_kind_d, P.var_stride_d, P.n_leaves, P.bits_d, P.slice_d,
-        P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
-    g_launches++;
-    pr.n_other++;
-    const size_t l0 = phase == 0 ? 0 : (size_t)P.n_pro, l1 = phase == 0 ? (size_t)P.n_pro : P.launches.size();
-    for (size_t li = l0; li < l1; ++li) {
-      const auto& L = P.launches[li];
-      if (L.first == 0) {
-        {
-          const auto& w = P.waves[L.second];
-          size_t big = 0;
-          for (size_t q = 1; q < w.steps.size(); ++q) {
-            const auto &x = w.steps[q], &y = w.steps[big];
-            if (x.nb_bits + x.m_bits + x.n_bits + x.k_bits > y.nb_bits + y.m_bits + y.n_bits + y.k_bits) big = q;
-          }
-          const auto& d = w.steps[big];
-          mk.mark(st, 0, TN_K_SMALL, profile_dump_ms() >= 0 ? shape_tag(("wave of " + std::to_string(w.steps.size()) + ", largest").c_str(),
-                                                           d.nb_bits, d.m_bits, d.n_bits, d.k_bits) : "");
+// one phase (0: prologue, 1: the slice at *slice_d) issued on `st` with CUDA event marks
+// around every kernel class; its algorithmic flops / bytes and counts are ADDED to stat
+void record_profiled(tn_plan_s& P, int phase, cudaStream_t st, Marks& mk, tn_profile& stat) {
+  mk.mark(st, 4, TN_K_OTHER);
+  tnd::set_leaf_ptrs_kernel<<<(P.n_leaves + 127) / 128, 128, 0, st>>>(
+      P.ptrs_d, P.leaf_base_d, P.var_begin_d, P.var_kind_d, P.var_stride_d, P.n_leaves, P.bits_d, P.slice_d,
+      P.sl_log2_d, P.sl_shift_d, P.esz, P.leaves);
+  g_launches++;
+  stat.n_other++;
+  const size_t l0 = phase == 0 ? 0 : (size_t)P.n_pro, l1 = phase == 0 ? (size_t)P.n_pro : P.launches.size();
+  for (size_t li = l0; li < l1; ++li) {
+    const auto& L = P.launches[li];
+    if (L.first == 0) {
+      {
+        const auto& w = P.waves[L.second];
+        size_t big = 0;
+        for (size_t q = 1; q < w.steps.size(); ++q) {
+          const auto &x = w.steps[q], &y = w.steps[big];
+          if (x.nb_bits + x.m_bits + x.n_bits + x.k_bits > y.nb_bits + y.m_bits + y.n_bits + y.k_bits) big = q;
         }
-        if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
-        else launch_wave<double>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
-        pr.n_small++;
-        pr.flops_small += P.waves[L.second].flops;
-        pr.bytes_small += P.waves[L.second].bytes;
-        pr.k_flops[TN_K_SMALL] += P.waves[L.second].flops;
-        pr.k_bytes[TN_K_SMALL] += P.waves[L.second].bytes;
+        const auto& d = w.steps[big];
+        mk.mark(st, 0, TN_K_SMALL, profile_dump_ms() >= 0 ? shape_tag(("wave of " + std::to_string(w.steps.size()) + ", largest").c_str(),
+                                                         d.nb_bits, d.m_bits, d.n_bits, d.k_bits) : "");
+      }
+      if (P.dtype == TN_C64) launch_wave<float>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
+      else launch_wave<double>(P.waves[L.second], P.ptrs_d, P.tab_d, st);
+      stat.n_small++;
+      stat.flops_small += P.waves[L.second].flops;
+      stat.bytes_small += P.waves[L.second].bytes;
+      stat.k_flops[TN_K_SMALL] += P.waves[L.second].flops;
+      stat.k_bytes[TN_K_SMALL] += P.waves[L.second].bytes;
+    } else {
+      const auto& t = P.tcs[L.second];
+      launch_tc(t, P.arena, P.ptrs_d, P.tab_d, st, &mk);
+      const double ex = std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits), ey = std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits);
+      stat.n_pack += 2 * t.n_slabs;
+      // algorithmic bytes: a planar pack reads and writes every entry once (2 esz per
+      // entry); the fp16x2 pack reads 8 and writes 8 bytes per entry plus one fp32
+      // scale per 128-entry K chunk; skinny / wide read both planar operands and write C
+      if (t.kind == K_SKINNY || t.kind == K_WIDE) {   // CUDA-core: accounted with the small path
+        const double b = t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
+        stat.n_small += t.n_slabs;
+        stat.flops_small += t.flops;
+        stat.bytes_small += b;
+        if (!t.gather) stat.bytes_pack += 2.0 * t.esz * (ex + ey);
+        const int kc = t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE;
+        stat.k_flops[kc] += t.flops;
+        stat.k_bytes[kc] += b;
+        if (!t.gather) stat.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
       } else {
-        const auto& t = P.tcs[L.second];
-        launch_tc(t, P.arena, P.ptrs_d, P.tab_d, st, &mk);
-        const double ex = std::ldexp(1.0, t.nb_bits + t.m_bits + t.k_bits), ey = std::ldexp(1.0, t.nb_bits + t.n_bits + t.k_bits);
-        pr.n_pack += 2 * t.n_slabs;
-        // algorithmic bytes: a planar pack reads and writes every entry once (2 esz per
-        // entry); the fp16x2 pack reads 8 and writes 8 bytes per entry plus one fp32
-        // scale per 128-entry K chunk; skinny / wide read both planar operands and write C
-        if (t.kind == K_SKINNY || t.kind == K_WIDE) {   // CUDA-core: accounted with the small path
-          const double b = t.esz * (ex + ey + std::ldexp(1.0, t.nb_bits + t.m_bits + t.n_bits));
-          pr.n_small += t.n_slabs;
-          pr.flops_small += t.flops;
-          pr.bytes_small += b;
-          if (!t.gather) pr.bytes_pack += 2.0 * t.esz * (ex + ey);
-          const int kc = t.kind == K_SKINNY ? TN_K_SKINNY : TN_K_WIDE;
-          pr.k_flops[kc] += t.flops;
-          pr.k_bytes[kc] += b;
-          if (!t.gather) pr.k_bytes[TN_K_PACK_PLANAR] += 2.0 * t.esz * (ex + ey);
-        } else {
-          const double pb = t.gather ? 0.0 : (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
-          pr.n_gemm += t.n_slabs * t.n_mslabs;
-          pr.n_pack += t.n_mslabs - 1;
-          pr.flops_gemm += t.flops;
-          pr.bytes_pack += pb;
-          pr.k_flops[t.kind == K_DMMA ? TN_K_DMMA : gemm_class(t)] += t.flops;
-          pr.k_bytes[t.kind == K_DMMA ? TN_K_PACK_PLANAR : TN_K_PACK_TC] += pb;
-        }
+        const double pb = t.gather ? 0.0 : (t.kind == K_DMMA ? 32.0 : 16.0 + 4.0 / 128.0) * (ex + ey);
+        stat.n_gemm += t.n_slabs * t.n_mslabs;
+        stat.n_pack += t.n_mslabs - 1;
+        stat.flops_gemm += t.flops;
+        stat.bytes_pack += pb;
+        stat.k_flops[t.kind == K_DMMA ? TN_K_DMMA : gemm_class(t)] += t.flops;
+        stat.k_bytes[t.kind == K_DMMA ? TN_K_PACK_PLANAR : TN_K_PACK_TC] += pb;
       }
     }
-    if (phase == 1) {
-      mk.mark(st, 4, TN_K_OTHER);
-      if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
-      else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
-      g_launches++;
-      pr.n_other++;
-    }
-    mk.mark(st, -1, TN_K_OTHER);
-    CK(cudaEventSynchronize(mk.v.back().first));
-    for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, mk.v[j].first, mk.v[j + 1].first));
-      if (profile_dump_ms() >= 0 && ms > profile_dump_ms())
-        fprintf(stderr, "[tn profile] %8.3f ms  cat %d  %s\n", ms, mk.v[j].second, mk.tags[j].c_str());
-      if (mk.fine[j] >= 0 && mk.fine[j] < TN_K_COUNT) {
-        pr.k_ms[mk.fine[j]] += ms;
-        pr.k_intervals[mk.fine[j]]++;
-      }
-      switch (mk.v[j].second) {
-        case 0: pr.ms_small += ms; break;
-        case 1: pr.ms_pack += ms; break;
-        case 2: pr.ms_gemm += ms; break;
-        case 3: pr.ms_other += ms; break;     // split-K reduction
-        default: pr.ms_other += ms; break;
-      }
-    }
-    for (auto& e : mk.v) cudaEventDestroy(e.first);
   }
+  if (phase == 1) {
+    mk.mark(st, 4, TN_K_OTHER);
+    if (P.dtype == TN_C64) tnd::accumulate_root_kernel<float><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
+    else tnd::accumulate_root_kernel<double><<<1, 1, 0, st>>>(P.ptrs_d, P.root, P.root_exp, P.amp_d, P.slice_d);
+    g_launches++;
+    stat.n_other++;
+  }
+  mk.mark(st, -1, TN_K_OTHER);
+}
+
+// device times between consecutive marks (all recorded), ADDED to pr
+void read_marks(const Marks& mk, tn_profile& pr) {
+  for (size_t j = 0; j + 1 < mk.v.size(); ++j) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, mk.v[j].first, mk.v[j + 1].first));
+    if (profile_dump_ms() >= 0 && ms > profile_dump_ms())
+      fprintf(stderr, "[tn profile] %8.3f ms  cat %d  %s\n", ms, mk.v[j].second, mk.tags[j].c_str());
+    if (mk.fine[j] >= 0 && mk.fine[j] < TN_K_COUNT) {
+      pr.k_ms[mk.fine[j]] += ms;
+      pr.k_intervals[mk.fine[j]]++;
+    }
+    switch (mk.v[j].second) {
+      case 0: pr.ms_small += ms; break;
+      case 1: pr.ms_pack += ms; break;
+      case 2: pr.ms_gemm += ms; break;
+      case 3: pr.ms_other += ms; break;     // split-K reduction
+      default: pr.ms_other += ms; break;
+    }
+  }
+}
+
+void add_profile(tn_profile& a, const tn_profile& b) {
+  a.ms_small += b.ms_small; a.ms_pack += b.ms_pack; a.ms_gemm += b.ms_gemm; a.ms_other += b.ms_other;
+  a.flops_gemm += b.flops_gemm; a.flops_small += b.flops_small;
+  a.bytes_small += b.bytes_small; a.bytes_pack += b.bytes_pack;
+  a.n_gemm += b.n_gemm; a.n_pack += b.n_pack; a.n_small += b.n_small; a.n_other += b.n_other;
+  for (int k = 0; k < 16; ++k) {
+    a.k_ms[k] += b.k_ms[k]; a.k_flops[k] += b.k_flops[k]; a.k_bytes[k] += b.k_bytes[k];
+    a.k_intervals[k] += b.k_intervals[k];
+  }
+}
+
+// TN_PROFILE_GRAPH=0: profiled calls launch eagerly instead of replaying the profiled graphs
+bool profile_graph_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TN_PROFILE_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// one profiled phase, timings ADDED to pr: by default a replay of the phase's profiled CUDA
+// graph -- the same launches as the plan's graph with event records between the kernel
+// classes, captured once per plan -- so the timed launches have the production path's
+// (graph) launch gaps; eagerly (launch by launch) with TN_PROFILE_GRAPH=0 or if the capture
+// failed
+void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
+  auto& G = P.prof_graph[phase];
+  if (profile_graph_enabled() && !G.failed) {
+    if (!G.exec) {
+      cudaGraph_t g = nullptr;
+      const int64_t before = g_launches.load();
+      try {
+        CK(cudaStreamBeginCapture(P.cap, cudaStreamCaptureModeThreadLocal));
+        record_profiled(P, phase, P.cap, G.mk, G.stat);
+        CK(cudaStreamEndCapture(P.cap, &g));
+        CK(cudaGraphInstantiate(&G.exec, g, 0));
+        CK(cudaGraphDestroy(g));
+        G.kernels = g_launches.load() - before;
+      } catch (const Err&) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(P.cap, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaGetLastError();
+        G.failed = true;
+        G.reset();
+      }
+      g_launches = before;   // captured launches are counted when replayed
+    }
+    if (!G.failed) {
+      CK(cudaGraphLaunch(G.exec, st));
+      g_launches += G.kernels;
+      CK(cudaStreamSynchronize(st));
+      read_marks(G.mk, pr);
+      add_profile(pr, G.stat);
+      return;
+    }
+  }
+  Marks mk;
+  tn_profile stat;
+  std::memset(&stat, 0, sizeof(stat));
+  record_profiled(P, phase, st, mk, stat);
+  CK(cudaEventSynchronize(mk.v.back().first));
+  read_marks(mk, pr);
+  add_profile(pr, stat);
+  for (auto& e : mk.v) cudaEventDestroy(e.first);
 }
 
 // eager, profiled: the prologue (if asked and the plan has one), then slices [s0, s1)

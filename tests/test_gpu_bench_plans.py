@@ -1,7 +1,8 @@
 """The benched plans and the benched code path (-m gpu; VERDICT r1 "verify the benched
 plans").
 
-* tn_contract_profiled (the launcher bench.py times: eager launches with CUDA events) is
+* tn_contract_profiled (the launcher bench.py times: a profiled CUDA graph with event records;
+  eager launches with TN_PROFILE_GRAPH=0) is
   bit-identical to tn_contract_device (the CUDA-graph path) and accounts every flop;
 * configs[1], [2], [4] at full size with the bench's kernels (K-slabs / row slabs, CTA
   pairs, persistent tiles, K-chunks at the 2^30-entry pack cap): one slice of an order at
@@ -64,6 +65,19 @@ def test_profiled_path_matches_graph_path(dtype):
     assert torch.equal(a_prof, a_graph)
     assert abs(flops - info["flops_per_slice"] * ns) <= 1e-12 * flops
     assert abs(a_graph.sum().item() - plan.contract(x)) <= 1e-12 * abs(a_graph.sum().item()) + 1e-300
+
+
+def test_profiled_eager_path_matches_graph_path():
+    """TN_PROFILE_GRAPH=0 (child process): the profiled launcher's eager fallback, the same
+    checks as above in both dtypes."""
+    import subprocess, sys
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+            "import test_gpu_bench_plans as T, paper_2208_01498_b200 as tb\n"
+            "for dt in (tb.TN_C64, tb.TN_C128):\n    T.test_profiled_path_matches_graph_path(dt)\n"
+            "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env=dict(os.environ, TN_PROFILE_GRAPH="0"), cwd=ROOT)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 _C64_VS_C128 = textwrap.dedent("""
