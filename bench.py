@@ -18,9 +18,11 @@ partial amplitudes summed over ranks by ONE all-reduce (NCCL) inside the timed r
 --config 3 (IQP 10x10, complex128 on the FP64 tensor pipe): one STEP = one full
 amplitude (unsliced), contiguous blocks of the 256 bitstrings per rank.
 
-The timed steps go through tn_contract_profiled (eager launches, CUDA events per kernel
-class); their per-step amplitudes are checked against the CUDA-graph path
-(tn_contract_device) for the same (bitstring, slice) after the timed region.
+The timed steps go through tn_prepare / tn_contract_prepared with a profile: each replays
+a profiled CUDA graph (the plan's launches with CUDA event records between the kernel
+classes) in deferred mode (tn_profile_defer: no wait per call; the device times are
+collected by tn_profile_collect after the region); their per-step amplitudes are checked
+against the unprofiled CUDA-graph path for the same (bitstring, slice) afterwards.
 
 --impl reference: the oracle (numpy complex128, oracle/) on the host cores, along the
 oracle's own order for the workload (oracle/orders/config<C>.json, written by
@@ -421,6 +423,10 @@ def run_ours(args):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev = {"pro": [], "slice": []}
+    # profiled calls in deferred mode: each replays a profiled CUDA graph without waiting
+    # for it (the per-kernel-class device times are collected after the region), so the
+    # host keeps the GPU fed as in the unprofiled graph path
+    plan.profile_defer(True)
     with Clocks(local) as clk:
         e0.record(stream)
         profs, n_pre = run(items, amp, True, ev)
@@ -429,6 +435,8 @@ def run_ours(args):
             pdist.allreduce_sum_(amp)               # partial amplitudes of all ranks' slices
         e1.record(stream)
         barrier()
+    profs.append(plan.profile_collect())            # the device times of the deferred replays
+    plan.profile_defer(False)
     launches = tb.kernel_launches() - launches0
     prof = profs[0]
     for p in profs[1:]:

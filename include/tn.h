@@ -220,6 +220,16 @@ typedef struct {
 } tn_profile;
 int tn_contract_profiled(tn_plan plan, const uint8_t* bits_dev, int64_t slice_begin, int64_t slice_end,
                          void* amp_dev, void* stream, tn_profile* prof);
+/* tn_profile_defer: with on != 0 the profiled calls on `plan` (tn_contract_profiled,
+ * tn_prepare / tn_contract_prepared with a profile) do not wait for their kernels: each
+ * replays one of two profiled graphs per phase (reading the device times of that graph's
+ * previous replay first) and returns only the algorithmic flops / bytes and counts; the
+ * device times of all deferred replays are summed in the plan until tn_profile_collect
+ * waits for the outstanding ones and returns them (times only: ms_*, k_ms, k_intervals),
+ * clearing the sum.  So a loop of profiled calls keeps the GPU busy (bench.py's timed
+ * region).  Eager profiling (TN_PROFILE_GRAPH=0) stays synchronous. */
+int tn_profile_defer(tn_plan plan, int32_t on);
+int tn_profile_collect(tn_plan plan, tn_profile* prof);
 /* Slice reuse across calls (PAPER.md l.178 index slicing):
  * tn_contract / tn_contract_device / tn_contract_profiled / tn_amplitudes run the
  * bitstring's slice-invariant prologue once per call, then the slices.  To spread the

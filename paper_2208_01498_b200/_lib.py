@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "tn_last_error", "tn_version", "tn_build_network", "tn_network_free", "tn_network_get_info",
     "tn_network_dims", "tn_network_tensor", "tn_order_params_default", "tn_find_order", "tn_order_free",
     "tn_order_get_info", "tn_order_steps", "tn_order_slices", "tn_order_import", "tn_plan_create", "tn_plan_free",
-    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_prepare", "tn_contract_prepared", "tn_amplitudes", "tn_contract_pair",
+    "tn_plan_get_info", "tn_plan_steps", "tn_plan_set_lanes", "tn_contributing_slices", "tn_contributing_slice_ids", "tn_contract", "tn_contract_device", "tn_contract_profiled", "tn_profile_defer", "tn_profile_collect", "tn_prepare", "tn_contract_prepared", "tn_amplitudes", "tn_contract_pair",
     "tn_kernel_launches",
 ]
 
@@ -95,6 +95,8 @@ def _load():
         "tn_contract_device": (C.c_int, [P, P, I64, I64, P, P]),
         "tn_contract_profiled": (C.c_int, [P, P, I64, I64, P, P, C.POINTER(Profile)]),
         "tn_prepare": (C.c_int, [P, P, P, C.POINTER(Profile)]),
+        "tn_profile_defer": (C.c_int, [P, I32]),
+        "tn_profile_collect": (C.c_int, [P, C.POINTER(Profile)]),
         "tn_contract_prepared": (C.c_int, [P, I64, I64, P, P, C.POINTER(Profile)]),
         "tn_amplitudes": (C.c_int, [P, P, I32, P, P]),
         "tn_contract_pair": (C.c_int, [I32, P, I32, P, P, I32, P, P, I32, P, P, I32, I32, P]),
@@ -297,6 +299,18 @@ class Plan:
                                  "intervals": int(pr.k_intervals[i])}
                           for i, name in enumerate(KERNEL_CLASSES)}
         return out
+
+    def profile_defer(self, on=True):
+        """tn_profile_defer: profiled calls stop waiting for their kernels; their device
+        times are collected by profile_collect()."""
+        _check(lib.tn_profile_defer(self.h, 1 if on else 0))
+
+    def profile_collect(self):
+        """tn_profile_collect: waits for the deferred profiled replays, returns their summed
+        device times (profile dict, flops / bytes zero)."""
+        pr = Profile()
+        _check(lib.tn_profile_collect(self.h, C.byref(pr)))
+        return self._profile_dict(pr)
 
     def prepare(self, bits_dev_ptr, stream=0, profiled=False):
         """tn_prepare: the bitstring's slice-invariant prologue (profile dict if profiled)."""

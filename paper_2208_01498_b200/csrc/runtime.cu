@@ -1144,6 +1144,7 @@ struct tn_plan_s {
     tn_profile stat{};
     int64_t kernels = 0;
     bool failed = false;
+    bool pending = false;           // deferred mode: replayed, its times not read yet
     void reset() {
       if (exec) cudaGraphExecDestroy(exec);
       exec = nullptr;
@@ -1152,7 +1153,10 @@ struct tn_plan_s {
       stat = tn_profile{};
     }
   };
-  ProfGraph prof_graph[2];
+  ProfGraph prof_graph[2][2];       // [phase][buffer]: two per phase for deferred replays
+  bool prof_defer = false;          // tn_profile_defer: profiled calls do not wait
+  int prof_buf[2] = {0, 0};         // next buffer per phase (deferred mode)
+  tn_profile prof_acc{};            // device times of deferred replays read so far
   bool prepared = false;            // tn_prepare ran and no other contraction call since
   int64_t n_slices = 1;
   int slice_bits = 0;
@@ -1264,7 +1268,8 @@ struct tn_plan_s {
     }
     if (graph) cudaGraphExecDestroy(graph);
     if (graph_pro) cudaGraphExecDestroy(graph_pro);
-    for (auto& g : prof_graph) g.reset();
+    for (auto& ph : prof_graph)
+      for (auto& g : ph) g.reset();
     if (cap) cudaStreamDestroy(cap);
     for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
     for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
@@ -1864,7 +1869,12 @@ bool profile_graph_enabled() {
 // (graph) launch gaps; eagerly (launch by launch) with TN_PROFILE_GRAPH=0 or if the capture
 // failed
 void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
-  auto& G = P.prof_graph[phase];
+  // deferred mode (tn_profile_defer): alternate two profiled graphs per phase, read the
+  // times of a buffer's previous replay (two calls back) before replaying it again, return
+  // only the algorithmic counters now -- the host never waits on the call in flight
+  const int buf = P.prof_defer ? P.prof_buf[phase] : 0;
+  if (P.prof_defer) P.prof_buf[phase] ^= 1;
+  auto& G = P.prof_graph[phase][buf];
   if (profile_graph_enabled() && !G.failed) {
     if (!G.exec) {
       cudaGraph_t g = nullptr;
@@ -1887,10 +1897,19 @@ void profile_phase(tn_plan_s& P, int phase, cudaStream_t st, tn_profile& pr) {
       g_launches = before;   // captured launches are counted when replayed
     }
     if (!G.failed) {
+      if (G.pending) {          // deferred: this buffer's previous replay
+        CK(cudaEventSynchronize(G.mk.v.back().first));
+        read_marks(G.mk, P.prof_acc);
+        G.pending = false;
+      }
       CK(cudaGraphLaunch(G.exec, st));
       g_launches += G.kernels;
-      CK(cudaStreamSynchronize(st));
-      read_marks(G.mk, pr);
+      if (P.prof_defer) {
+        G.pending = true;
+      } else {
+        CK(cudaStreamSynchronize(st));
+        read_marks(G.mk, pr);
+      }
       add_profile(pr, G.stat);
       return;
     }
@@ -2277,6 +2296,31 @@ int tn_contract_prepared(tn_plan p, int64_t slice_begin, int64_t slice_end, void
     add_amp_kernel<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(amp_dev), p->amp_d);
     g_launches++;
     CK(cudaGetLastError());
+  });
+}
+
+int tn_profile_defer(tn_plan p, int32_t on) {
+  return guard([&] {
+    if (!p) throw Err(TN_EINVAL, "null");
+    CK(cudaSetDevice(p->device));
+    p->prof_defer = on != 0;
+  });
+}
+
+int tn_profile_collect(tn_plan p, tn_profile* prof) {
+  return guard([&] {
+    if (!p || !prof) throw Err(TN_EINVAL, "null");
+    CK(cudaSetDevice(p->device));
+    for (auto& ph : p->prof_graph)
+      for (auto& g : ph)
+        if (g.pending) {
+          CK(cudaEventSynchronize(g.mk.v.back().first));
+          read_marks(g.mk, p->prof_acc);
+          g.pending = false;
+        }
+    std::memset(prof, 0, sizeof(*prof));
+    add_profile(*prof, p->prof_acc);
+    p->prof_acc = tn_profile{};
   });
 }
 

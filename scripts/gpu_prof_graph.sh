@@ -2,7 +2,7 @@
 # and configs[1] bench A/B (TN_PROFILE_GRAPH = 1 / 0)
 set -x
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 1500 python -m pytest tests/test_gpu_bench_plans.py tests/test_dist_gpu.py -x -q -m gpu -k "profiled or reuse or two_ranks" 2>&1 | tail -3
+timeout 1500 python -m pytest tests/test_gpu_bench_plans.py tests/test_dist_gpu.py -x -q -m gpu -k "profiled or reuse or two_ranks or deferred" 2>&1 | tail -3
 for v in 1 0 1 0; do
   TN_PROFILE_GRAPH=$v timeout 600 python bench.py --config 3 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/b3_pg$v.json 2> gpurun_out/b3_pg$v.err
   python -c "

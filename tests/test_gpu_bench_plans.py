@@ -216,3 +216,38 @@ def test_slice_reuse_prologue():
                        env=dict(os.environ, TN_SLICE_REUSE="0"))
     assert r.returncode == 0, r.stdout + r.stderr
     assert eval(r.stdout.strip().splitlines()[-1]) == [complex(a) for a in plan.amplitudes(xs)]
+
+
+def test_deferred_profiling_matches_synchronous():
+    """tn_profile_defer / tn_profile_collect (bench.py's timed region): a loop of deferred
+    profiled slices gives the same amplitudes as the graph path, per-call algorithmic
+    counters as in synchronous mode, and device times for every kernel class that ran
+    (collected once at the end; a second collect returns nothing)."""
+    dev = _cuda()
+    c = sycamore(6, 3)
+    net = tb.Network.from_circuit(c)
+    plan = tb.Plan(net, tb.Order(net, seed=0, max_log2_size=16), dtype=tb.TN_C64)
+    ns = plan.info()["n_slices"]
+    x = random_bitstrings(c.n, 1, 5)[0]
+    bits = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    st = torch.cuda.current_stream().cuda_stream
+    a_sync = torch.zeros(ns, dtype=torch.complex128, device=dev)
+    a_def = torch.zeros(ns, dtype=torch.complex128, device=dev)
+    sync = [plan.contract_profiled(bits.data_ptr(), s, s + 1, a_sync[s:s + 1].data_ptr(), st) for s in range(ns)]
+    plan.profile_defer(True)
+    defer = [plan.contract_profiled(bits.data_ptr(), s, s + 1, a_def[s:s + 1].data_ptr(), st) for s in range(ns)]
+    col = plan.profile_collect()
+    plan.profile_defer(False)
+    again = plan.profile_collect()
+    torch.cuda.synchronize()
+    assert torch.equal(a_sync, a_def)
+    for p, q in zip(sync, defer):
+        for name in p["kernels"]:
+            assert p["kernels"][name]["flops"] == q["kernels"][name]["flops"]
+            assert p["kernels"][name]["bytes"] == q["kernels"][name]["bytes"]
+            assert q["kernels"][name]["ms"] == 0.0
+    for name, d in col["kernels"].items():
+        n_sync = sum(p["kernels"][name]["intervals"] for p in sync)
+        assert d["intervals"] == n_sync, name
+        assert (d["ms"] > 0) == (n_sync > 0), name
+    assert all(d["intervals"] == 0 and d["ms"] == 0 for d in again["kernels"].values())
