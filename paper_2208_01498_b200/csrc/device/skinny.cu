@@ -754,32 +754,42 @@ __global__ void __launch_bounds__(BS_THREADS) bskinny_kernel(const GatherMaps gm
   // with more than one range the CTA writes partial[b][range][o] (summed in order by
   // skinny_reduce_*_kernel) instead of C
   const int64_t KR = K >> s_bits;
+  // per CTA: the row offsets inside a batch and -- when one chunk is a whole K range of
+  // every item -- the K offsets; per item only the two batch offsets are looked up
+  for (int r = threadIdx.x; r < M + N; r += BS_THREADS) {
+    if (r < M) rowX[r] = gmap(tab, gm.Am, r);
+    else rowY[r - M] = gmap(tab, gm.Bn, r - M);
+  }
+  const bool kfixed = s_bits == 0 && KC == K;
+  if (kfixed)
+    for (int k = threadIdx.x; k < KC; k += BS_THREADS) {
+      kX[k] = gmap(tab, gm.Ak, k);
+      kY[k] = gmap(tab, gm.Bk, k);
+    }
   for (int64_t item = blockIdx.x; item < (n_batches << s_bits); item += gridDim.x) {
     const int64_t b = item >> s_bits, kr = item & ((int64_t(1) << s_bits) - 1);
-    __syncthreads();                                          // the previous item's reads are done
-    for (int r = threadIdx.x; r < M + N; r += BS_THREADS) {
-      if (r < M) rowX[r] = gmap(tab, gm.Ab, b) + gmap(tab, gm.Am, r);
-      else rowY[r - M] = gmap(tab, gm.Bb, b) + gmap(tab, gm.Bn, r - M);
-    }
+    const int64_t xb = gmap(tab, gm.Ab, b), yb = gmap(tab, gm.Bb, b);
     double re = 0.0, im = 0.0;
     for (int64_t k0 = kr * KR; k0 < (kr + 1) * KR; k0 += KC) {
-      __syncthreads();                                        // rows ready / previous chunk consumed
-      for (int k = threadIdx.x; k < KC; k += BS_THREADS) {
-        kX[k] = gmap(tab, gm.Ak, k0 + k);
-        kY[k] = gmap(tab, gm.Bk, k0 + k);
+      __syncthreads();                      // offsets ready; the previous chunk / item consumed
+      if (!kfixed) {
+        for (int k = threadIdx.x; k < KC; k += BS_THREADS) {
+          kX[k] = gmap(tab, gm.Ak, k0 + k);
+          kY[k] = gmap(tab, gm.Bk, k0 + k);
+        }
+        __syncthreads();
       }
-      __syncthreads();
       // gather along the operand's stride-1 direction (K or rows) so a warp's loads
       // coalesce; cp.async straight to shared memory (every element's load in flight at once)
       for (int e = threadIdx.x; e < M * KC; e += BS_THREADS) {
         const int r = gm.a_kfast ? e >> kc_bits : e & (M - 1);
         const int k = gm.a_kfast ? e & (KC - 1) : e >> m_bits;
-        bs_cp_async(&xs[k * MP + r], &A[rowX[r] + kX[k]]);
+        bs_cp_async(&xs[k * MP + r], &A[xb + rowX[r] + kX[k]]);
       }
       for (int e = threadIdx.x; e < N * KC; e += BS_THREADS) {
         const int r = gm.b_kfast ? e >> kc_bits : e & (N - 1);
         const int k = gm.b_kfast ? e & (KC - 1) : e >> n_bits;
-        bs_cp_async(&ys[k * NP + r], &B[rowY[r] + kY[k]]);
+        bs_cp_async(&ys[k * NP + r], &B[yb + rowY[r] + kY[k]]);
       }
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       __syncthreads();
