@@ -794,13 +794,20 @@ __global__ void __launch_bounds__(BS_THREADS) bskinny_kernel(const GatherMaps gm
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       __syncthreads();
       // four independent accumulator pairs (k = j + G (4 i + u)) hide the FMA latency
+      // (all 8 shared loads of a group issued before its FMAs: the loop was bound by the
+      // shared-load latency, ncu stall_short_sb)
       double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
       int k = j;
       for (; k + 3 * G < KC; k += 4 * G) {
+        C2 x[4], y[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const C2 x = xs[(k + u * G) * MP + om], y = ys[(k + u * G) * NP + on];
-          const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+          x[u] = xs[(k + u * G) * MP + om];
+          y[u] = ys[(k + u * G) * NP + on];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double xr = x[u].x, xi = x[u].y, yr = y[u].x, yi = y[u].y;
           ar[u] = fma(xr, yr, fma(-xi, yi, ar[u]));
           ai[u] = fma(xr, yi, fma(xi, yr, ai[u]));
         }
