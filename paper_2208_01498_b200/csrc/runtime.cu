@@ -340,6 +340,8 @@ int64_t plane_bytes(const PackDesc& d) { return int64_t(8) << (d.nb_bits + d.r_b
 // fill the partial last wave of 64 x 64 tiles (configs[3]'s dominant step: 1024 tiles =
 // 3.46 waves of 296 slots), but the halved warp tile (one 16-row fragment per warp) costs
 // more than the tail: configs[3] 1.92 -> 1.96 ms per amplitude (measured), so 64 wide
+// (also measured per step: 64 x 32 tiles only for steps under one wave of 64 x 64 tiles,
+// configs[3]'s K = 256 steps, 0.096 -> 0.107 ms each: the tile count is not what limits them)
 bool dmma_bn32(const TcStep&) {
   static const bool v = [] {
     const char* e = std::getenv("TN_DMMA_BN");
