@@ -251,3 +251,42 @@ def test_deferred_profiling_matches_synchronous():
         assert d["intervals"] == n_sync, name
         assert (d["ms"] > 0) == (n_sync > 0), name
     assert all(d["intervals"] == 0 and d["ms"] == 0 for d in again["kernels"].values())
+
+
+def test_deferred_profiling_with_prologue():
+    """bench.py's timed loop on a plan with a slice-invariant prologue: tn_prepare and
+    tn_contract_prepared with profiles in deferred mode over two bitstrings (both
+    phases' profiled graphs alternate their two buffers) give bit-identical slice
+    amplitudes to the unprofiled graph path, and the collected device times cover the
+    prologue and every slice."""
+    dev = _cuda()
+    c = lattice_cz(6, 6, 12, 8)
+    net = tb.Network.from_circuit(c)
+    plan = tb.Plan(net, tb.Order(net, seed=0, max_log2_size=19), dtype=tb.TN_C64)
+    info = plan.info()
+    assert info["flops_prologue"] > 0
+    ns = info["n_slices"]
+    xs = random_bitstrings(c.n, 2, 8)
+    st = torch.cuda.current_stream().cuda_stream
+    want = torch.zeros(2 * ns, dtype=torch.complex128, device=dev)
+    got = torch.zeros(2 * ns, dtype=torch.complex128, device=dev)
+    bits = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in xs]
+    for r in range(2):
+        plan.prepare(bits[r].data_ptr(), st)
+        for s in range(ns):
+            plan.contract_prepared(s, s + 1, want[r * ns + s:r * ns + s + 1].data_ptr(), st)
+    plan.profile_defer(True)
+    flops = 0.0
+    for r in range(2):
+        p = plan.prepare(bits[r].data_ptr(), st, profiled=True)
+        flops += sum(d["flops"] for d in p["kernels"].values())
+        for s in range(ns):
+            p = plan.contract_prepared(s, s + 1, got[r * ns + s:r * ns + s + 1].data_ptr(), st, profiled=True)
+            flops += sum(d["flops"] for d in p["kernels"].values())
+    col = plan.profile_collect()
+    plan.profile_defer(False)
+    torch.cuda.synchronize()
+    assert torch.equal(want, got)
+    expect = 2 * info["flops_prologue"] + 2 * ns * (info["flops_per_slice"] - info["flops_prologue"])
+    assert abs(flops - expect) <= 1e-9 * expect
+    assert col["ms_gemm"] > 0 and col["kernels"]["other"]["intervals"] == 2 * 1 + 2 * ns * 2
