@@ -501,6 +501,16 @@ Sk2Shape skinny2_shape(const TcStep& t) {
   return h;
 }
 
+// TN_WIDE_FULLGRID=1: one CTA per wide tile (the block scheduler balances the SMs) instead
+// of a grid-stride loop over 8 CTAs per SM (A/B switch)
+bool wide_full_grid() {
+  static const bool on = [] {
+    const char* e = std::getenv("TN_WIDE_FULLGRID");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // complex64 wide steps (gathered, K = 16) with packed fp32 pairs (FFMA2); TN_WIDE_FFMA2=0: scalar FFMA
 bool wide_ffma2() {
   static const bool on = [] {
@@ -656,7 +666,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       const bool two = sizeof(R) == 4 && t.n_bits >= 1;
       const int64_t tm = std::min(tnd::wd_tm<R>(), 1 << t.m_bits), tn = int64_t(tnd::WD_THREADS) * (two ? 2 : 1);
       const int64_t tiles = (int64_t(1) << (t.nb_bits + t.m_bits)) / tm * (((int64_t(1) << t.n_bits) + tn - 1) / tn);
-      const unsigned grid = (unsigned)std::min<int64_t>(tiles, 148 * 8);
+      const unsigned grid = (unsigned)std::min<int64_t>(tiles, wide_full_grid() ? (int64_t(1) << 30) : 148 * 8);
 #define TN_WIDE(CPT, KB)                                                                                    \
   if (t.k_bits == KB) {                                                                                     \
     if (t.gather)                                                                                           \
@@ -876,13 +886,14 @@ struct Wave {
   std::vector<int64_t> prefix;
   SmallStep* steps_d = nullptr;
   int64_t* prefix_d = nullptr;
+  int32_t* cta_step_d = nullptr;    // CTA -> step (plans; nullptr: the kernel searches prefix)
   int64_t n_cta = 0;
 };
 
 template <typename R>
 void launch_wave(const Wave& w, void* const* ptrs_d, const int64_t* tab_d, cudaStream_t st) {
   tnd::small_contract_kernel<R><<<(unsigned)w.n_cta, 128, 0, st>>>(w.steps_d, w.prefix_d, (int)w.steps.size(), tab_d,
-                                                                     ptrs_d, OUTS_PER_CTA);
+                                                                     ptrs_d, w.cta_step_d);
   g_launches++;
   CK(cudaGetLastError());
 }
@@ -1273,7 +1284,7 @@ struct tn_plan_s {
     for (auto& ph : prof_graph)
       for (auto& g : ph) g.reset();
     if (cap) cudaStreamDestroy(cap);
-    for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); }
+    for (auto& w : waves) { cudaFree(w.steps_d); cudaFree(w.prefix_d); if (w.cta_step_d) cudaFree(w.cta_step_d); }
     for (void* p : {(void*)arena, (void*)leaves, (void*)tab_d, (void*)ptrs_d, (void*)leaf_base_d, (void*)var_begin_d,
                     (void*)var_kind_d, (void*)var_stride_d, (void*)sl_log2_d, (void*)sl_shift_d, (void*)bits_d,
                     (void*)slice_d, (void*)amp_d})
@@ -1711,6 +1722,12 @@ void build_plan(tn_plan_s& P, const tn::Network& net, const tn::Order& ord, bool
   for (auto& w : P.waves) {
     w.steps_d = upload(w.steps);
     w.prefix_d = upload(w.prefix);
+    if (w.n_cta <= (int64_t(1) << 22)) {
+      std::vector<int32_t> cs((size_t)w.n_cta);
+      for (size_t q = 0; q < w.steps.size(); ++q)
+        for (int64_t b = w.prefix[q]; b < w.prefix[q + 1]; ++b) cs[(size_t)b] = (int32_t)q;
+      w.cta_step_d = upload(cs);
+    }
   }
   if (n == 1 && ord.steps.empty()) P.root = 0;
   // ---- capture the prologue and one slice as CUDA graphs ----
