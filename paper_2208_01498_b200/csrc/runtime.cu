@@ -595,7 +595,7 @@ void launch_cuda_core(const TcStep& t, char* arena, void* const* ptrs_d, const i
       const int64_t nbat = int64_t(1) << t.nb_bits;
       const int sb = bskinny_s_bits(t);
       double2* partial = reinterpret_cast<double2*>(arena + t.p_off);
-      tnd::bskinny_kernel<R><<<(unsigned)std::min<int64_t>(nbat << sb, 148 * 4), tnd::BS_THREADS, smem, st>>>(
+      tnd::bskinny_kernel<R><<<(unsigned)std::min<int64_t>(nbat << sb, wide_full_grid() ? (int64_t(1) << 24) : 148 * 4), tnd::BS_THREADS, smem, st>>>(
           t.gmaps, tab_d, ptrs_d, t.c_node, t.m_bits, t.n_bits, t.k_bits, kcb, nbat, sb, partial);
       g_launches++;
       if (sb > 0) {
