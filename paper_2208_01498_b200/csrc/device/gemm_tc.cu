@@ -85,6 +85,8 @@ __device__ __forceinline__ void split2x2(float a, float b, uint32_t& p0, uint32_
 // [b][K / 128][r] fp32 (one per row and 128-element K chunk; one per row if K < 128).
 // Tiles have 2^t_bits elements, 8 <= t_bits <= PACK_MAX_T, destination bits 0..6 always
 // inside the tile, so every K chunk is held by 2-16 adjacent threads of one warp.
+// 4 CTAs per SM (64 registers, a few spilled) beat 3 without spills in the configs[1]
+// step: 0.73 vs 0.70 of the copy peak (more bytes in flight; scripts/gpu_pack_ab.sh)
 __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void* const* __restrict__ ptrs, PackDesc d,
                                                                    const int64_t* __restrict__ tab,
                                                                    __half* __restrict__ out, float* __restrict__ scales,
@@ -141,16 +143,24 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_f16x2s_kernel(const void
     for (int o = 1; o < (1 << (chunk_log2 - 3)); o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     int e = 0;
     frexpf(m, &e);                                       // m < 2^e (e = 0 for m = 0)
-    // scale up by 2^(14-e), exact; two factors when 14-e exceeds the fp32 exponent range
+    // scale up by 2^(14-e), exact; a second factor only when 14-e exceeds the fp32
+    // exponent range (chunk maxima below 2^-113: a warp-uniform, practically never taken
+    // branch -- the pack is issue-bound at the power-capped clock)
     const float upc = ldexpf(1.f, min(14 - e, 127));
-    const float up2 = ldexpf(1.f, max(14 - e - 127, 0));
+    if (14 - e > 127) {
+      const float up2 = ldexpf(1.f, 14 - e - 127);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        w[j].x *= up2; w[j].y *= up2; w[j].z *= up2; w[j].w *= up2;
+      }
+    }
     uint4 o[4];
     uint32_t* op = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t r0, r1, i0, i1;
-      split2x2(w[j].x * upc * up2, w[j].z * upc * up2, r0, r1);
-      split2x2(w[j].y * upc * up2, w[j].w * upc * up2, i0, i1);
+      split2x2(w[j].x * upc, w[j].z * upc, r0, r1);
+      split2x2(w[j].y * upc, w[j].w * upc, i0, i1);
       op[0 * 4 + j] = r0; op[1 * 4 + j] = i0; op[2 * 4 + j] = r1; op[3 * 4 + j] = i1;
     }
 #pragma unroll
