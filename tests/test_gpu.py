@@ -859,3 +859,46 @@ def test_plans_on_two_devices_when_present():
         assert plan.info()["n_steps_tc"] > 0
         got = plan.amplitudes(np.array([x]))[0]
         assert abs(got - want) <= 1e-5 * max(abs(want), 2.0 ** (-c.n / 2))
+
+
+GUARD_CASES = [
+    (tb.TN_PATH_SKINNY, 9, 2, 5, 9, 5),     # gathered skinny, chunked K
+    (tb.TN_PATH_SKINNY, 0, 0, 0, 14, 3),    # gathered skinny, K ranges + ordered reduction
+    (tb.TN_PATH_SKINNY, 1, 3, 2, 14, 8),    # gathered skinny, 2 batches x K ranges, permuted
+    (tb.TN_PATH_WIDE, 2, 5, 6, 2, 4),       # wide, one CTA per tile
+    (tb.TN_PATH_TC, 3, 9, 7, 8, 2),         # DMMA (complex128) / tcgen05 (complex64)
+    (tb.TN_PATH_SMALL, 2, 3, 3, 4, 1),      # small wave
+]
+
+
+@pytest.mark.parametrize("dtype", [tb.TN_C64, tb.TN_C128])
+@pytest.mark.parametrize("case", range(len(GUARD_CASES)))
+def test_pair_writes_stay_in_bounds(case, dtype):
+    """C is written exactly where it lives: the output sits between two guard bands of
+    4096 sentinel entries in one allocation; after the step every sentinel is intact and
+    every output element finite and within its bound of the oracle."""
+    dev = _cuda()
+    path, nb, m, n, k, ps = GUARD_CASES[case]
+    ia, ib, ic, dims = _gemm_case(nb, m, n, k, ps)
+    A = _rand([dims[i] for i in ia], 70 + case, dtype)
+    B = _rand([dims[i] for i in ib], 71 + case, dtype)
+    tdt = torch.complex64 if dtype == tb.TN_C64 else torch.complex128
+    sc = [dims[i] for i in ic]
+    n_c = int(np.prod(sc)) if sc else 1
+    G = 4096
+    buf = torch.full((n_c + 2 * G,), complex(1234.5, -6789.25), dtype=tdt, device=dev)
+    tA, tB = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+    torch.cuda.synchronize()
+    tb.contract_pair(dtype, tA.data_ptr(), ia, tB.data_ptr(), ib, buf[G:].data_ptr(), ic, dims, path)
+    torch.cuda.synchronize()
+    h = buf.cpu().numpy()
+    assert np.all(h[:G] == complex(1234.5, -6789.25)) and np.all(h[G + n_c:] == complex(1234.5, -6789.25))
+    got = h[G:G + n_c].reshape(sc) if sc else h[G:G + 1].reshape(())
+    ref_inds, ref = oracle_pair(list(ia), A.astype(np.complex128), list(ib), B.astype(np.complex128), ic, dims)
+    _, bound = oracle_pair(list(ia), np.abs(A).astype(np.complex128), list(ib), np.abs(B).astype(np.complex128), ic, dims)
+    perm = [ref_inds.index(i) for i in ic]
+    ref = np.transpose(ref, perm) if perm else ref
+    bound = np.abs(np.transpose(bound, perm) if perm else bound)
+    tol = (1e-12 if dtype == tb.TN_C128 else (tc_tol(1 << k) if path == tb.TN_PATH_TC else c64_tol(1 << min(k, 3))))
+    assert np.all(np.isfinite(got))
+    assert np.all(np.abs(got - ref) <= tol * bound + 1e-30)
