@@ -559,6 +559,9 @@ def test_config3_full_size_sampled_amplitudes():
     c = config_circuit(3)
     plan = _plan_vs_oracle(c, tb.TN_C128, seed=0, hyper=True, n_bits=1, with_zero=False)
     assert plan.info()["n_steps_tc"] >= 1
+    # the plan's steps went through the gathered DMMA, wide and gathered skinny kernels
+    paths = set(int(p) for p in plan.steps()[:, 0])
+    assert {tb.TN_PATH_TC, tb.TN_PATH_WIDE, tb.TN_PATH_SKINNY, tb.TN_PATH_SMALL} <= paths, paths
 
 
 # ------------------------------------------------ full-size config 1 ------

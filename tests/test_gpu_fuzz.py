@@ -66,7 +66,8 @@ def test_random_plans_match_oracle(case):
 
 def test_random_plans_covered_every_path():
     """the random plans above went through the small and tensor-core paths and slice reuse in
-    both dtypes, and through the (gathering) wide kernel"""
+    both dtypes, and through the (gathering) wide kernel (skinny steps need larger circuits:
+    configs[3]'s full-size plan test covers them)"""
     if not _SEEN:
         pytest.skip("random plans did not run")
     for dt in (tb.TN_C64, tb.TN_C128):
