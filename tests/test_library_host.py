@@ -53,6 +53,16 @@ def test_network_identical_to_oracle(ci):
     _compare_networks(config_circuit(ci), hyper=(ci == 3))
 
 
+@pytest.mark.parametrize("hyper", [False, True])
+def test_network_identical_asymmetric_diagonal_gates(hyper):
+    """Diagonal two-qubit gates that are not symmetric in their qubits (R1 bond-2 split,
+    R3 hyperedge): the product's split must give each qubit its own role, as the oracle's
+    (pinned to the state vector in tests/test_oracle.py) does."""
+    from test_oracle import small_circuits
+    c = [x for x in small_circuits() if x.name == "diag_asym"][0]
+    _compare_networks(c, hyper)
+
+
 @pytest.mark.parametrize("case", ["c0", "c3", "small_slice", "syc_small", "r3d_small"])
 def test_order_and_slices_bit_identical(case):
     if case == "c0":

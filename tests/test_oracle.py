@@ -38,6 +38,16 @@ def small_circuits():
     c3 = Circuit(5, np.vstack([c2.pos, [[5.0, 5.0]]]), name="idle")
     c3.gates = list(c2.gates) + [((4,), haar_unitary(rng, 2))]
     out.append(c3)
+    # asymmetric diagonal two-qubit gates diag(e^{i phi_ab}) (R1's bond-2 split, R3's
+    # hyperedge): CZ and controlled phases are symmetric in the two qubits, these are not,
+    # so a split that swapped the qubits' roles would go unnoticed without them
+    c4 = Circuit(6, np.array([(x, y) for y in range(2) for x in range(3)], dtype=float), name="diag_asym")
+    for t in range(4):
+        for q in range(6):
+            c4.add((q,), haar_unitary(rng, 2))
+        for a, b in ([(0, 1), (3, 4)], [(2, 1), (5, 4)], [(0, 3), (5, 2)], [(4, 1)])[t]:
+            c4.add((a, b), np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, 4))))
+    out.append(c4)
     return out
 
 
@@ -72,7 +82,7 @@ def test_golden_worked_examples(name, hyper):
         assert abs(got - want) < 1e-14, (bits, got, want)
 
 
-@pytest.mark.parametrize("ci", range(5))
+@pytest.mark.parametrize("ci", range(6))
 @pytest.mark.parametrize("hyper", [False, True])
 def test_network_matches_statevector(ci, hyper):
     c = small_circuits()[ci]
