@@ -710,6 +710,33 @@ def test_lanes_concurrent_amplitudes():
             assert abs(g - want) <= tol * max(abs(want), scale)
 
 
+def test_amplitudes_empty_batch_and_fewer_bitstrings_than_lanes():
+    """Edge cases of tn_amplitudes (include/tn.h): an empty batch returns no amplitudes
+    and leaves the plan usable; with more lanes than bitstrings (2 and 1 bitstrings on 4
+    lanes: idle lanes, and the n_bits < 2 single-lane route) the amplitudes are
+    bit-identical to the single-lane plan's and match the oracle."""
+    _cuda()
+    c = lattice_cz(5, 5, 8, 4)
+    on = build_network(c)
+    osteps, _ = find_order(on, seed=1, max_log2_size=12)
+    cn = tb.Network.from_circuit(c)
+    co = tb.Order(cn, seed=1, max_log2_size=12)
+    assert co.steps() == osteps
+    for lanes in (1, 4):
+        plan = tb.Plan(cn, co, dtype=tb.TN_C128)
+        bits = random_bitstrings(c.n, 2, 11)
+        single = plan.amplitudes(bits)
+        if lanes > 1:
+            plan.set_lanes(lanes)
+        empty = plan.amplitudes(np.zeros((0, c.n), np.uint8))
+        assert empty.shape == (0,) and empty.dtype == np.complex128
+        assert np.array_equal(plan.amplitudes(bits), single)
+        assert np.array_equal(plan.amplitudes(bits[:1]), single[:1])
+        for x, g in zip(bits, single):
+            want = contract_tree(on, osteps, x)
+            assert abs(g - want) <= 1e-10 * max(abs(want), 2.0 ** (-c.n / 2))
+
+
 def test_bench_plan_slice_self_consistent():
     """The bench's own plan (configs[1], best of 256 hierarchies, bench.SPEC's slicing
     target, 2^30-entry pack cap: K-slabs, row slabs, CTA pairs, persistent tiles) is
